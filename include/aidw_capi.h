@@ -1,0 +1,209 @@
+/*
+ * aidw_capi.h — the C-ABI drop-in boundary of the B200 AIDW library
+ * (libaidw_b200.so, built from paper_1601_05904_b200/csrc/).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this line.
+ * Every batch entry point replaces one function of the reference header
+ * library (proj/include/aidw/*.hpp) and is what a binding for that path
+ * (ctypes, cgo, JNI, or the C++ shim in include/aidw/*.hpp) calls.
+ *
+ * Conventions
+ *  - Host entry points take HOST pointers and copy to/from HBM inside the
+ *    call.  Entry points with the _device suffix take DEVICE pointers that
+ *    are already resident on the current CUDA device.
+ *  - Return value: AIDW_OK (0) or an aidw_status code.  When `err` is not
+ *    NULL it is filled with {code, index, message}; `index` is the smallest
+ *    failing query / point (the reference's first-failure rule,
+ *    executor.hpp:37-44), or -1.  Codes map 1:1 onto the reference's
+ *    exception types (std::invalid_argument, std::domain_error,
+ *    std::out_of_range, std::runtime_error); CUDA failures are AIDW_ERR_CUDA.
+ *  - All functions are reentrant; each call uses its own stream unless one
+ *    is passed.  Results never depend on threading or GPU count.
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    entry point fails with AIDW_ERR_CUDA.
+ */
+#ifndef AIDW_CAPI_H
+#define AIDW_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AIDW_CAPI_VERSION 1
+
+typedef enum {
+    AIDW_OK = 0,
+    AIDW_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    AIDW_ERR_DOMAIN = 2,           /* std::domain_error     */
+    AIDW_ERR_OUT_OF_RANGE = 3,     /* std::out_of_range     */
+    AIDW_ERR_RUNTIME = 4,          /* std::runtime_error (per-query wrap) */
+    AIDW_ERR_CUDA = 5              /* device / driver failure             */
+} aidw_status;
+
+typedef struct {
+    int32_t code;
+    int64_t index;
+    char message[512];
+} aidw_error;
+
+/* GridConfig, proj/include/aidw/grid.hpp:24-34 */
+typedef struct {
+    double cell_width;
+    int32_t n_col;
+    int32_t n_row;
+    double min_x;
+    double min_y;
+} aidw_grid_config;
+
+/* AidwParams, proj/include/aidw/types.hpp:91-115 */
+typedef struct {
+    int32_t k;
+    double r_min;
+    double r_max;
+    double alpha_levels[5];
+    double area; /* <= 0: bbox(data ∪ queries) area */
+} aidw_params;
+
+enum { AIDW_ENGINE_GRID = 0, AIDW_ENGINE_BRUTE = 1 };     /* KnnEngine, knn.hpp:45          */
+enum { AIDW_VARIANT_NAIVE = 0, AIDW_VARIANT_BLOCKED = 1 }; /* Variant, interpolate.hpp:50   */
+enum { AIDW_MODE_IDW = 0, AIDW_MODE_AIDW = 1 };           /* cli::Mode, cli.hpp:26          */
+
+/* Weighting precision of Variant::blocked.  FP32 (default) is the MUFU
+ * kernel with the 1e-5 contract; FP64 routes blocked to the FP64 kernel
+ * (index-order, pow), as Variant::naive and pinned_order always are.  The
+ * environment variable AIDW_WEIGHT_FP64=1 sets FP64 at library load. */
+enum { AIDW_PRECISION_FP32 = 0, AIDW_PRECISION_FP64 = 1 };
+
+/* RunConfig, proj/include/aidw/cli.hpp:30-43 (file paths and seed omitted:
+ * they belong to the CLI, not to the pipeline). */
+typedef struct {
+    int32_t mode;      /* AIDW_MODE_*    */
+    int32_t engine;    /* AIDW_ENGINE_*  */
+    int32_t variant;   /* AIDW_VARIANT_* */
+    aidw_params params;
+    double alpha;       /* constant exponent, idw mode */
+    double cell_factor; /* cell width = factor * expected NN distance */
+    int32_t workers;    /* accepted and ignored (CPU threading knob) */
+    /* B200 additions (zero-initialise for reference behaviour): */
+    int32_t use_bbox;   /* 1: take bbox[] as bbox(data ∪ queries) — used by
+                           query-sharded multi-GPU runs so every rank sees
+                           the global box (identical grid, area, snap) */
+    double bbox[4];     /* min_x, min_y, max_x, max_y */
+} aidw_run_config;
+
+/* StageTimings, proj/include/aidw/executor.hpp:137-150, plus device detail. */
+typedef struct {
+    double build_ms;   /* grid build (K1), CUDA events              */
+    double knn_ms;     /* query sort + kNN + alpha (K2+K3)          */
+    double interp_ms;  /* weighting stage (K4 + settle)             */
+    double total_ms;   /* whole call incl. host<->device copies      */
+    double weight_kernel_ms; /* K4 launches only (roofline numerator) */
+    double knn_kernel_ms;    /* K2 launch only                        */
+    double h2d_ms, d2h_ms;
+    int32_t k_effective;
+    int32_t worker_count;
+    int64_t pairs;           /* m * n weighting pairs evaluated        */
+    int64_t knn_candidates;  /* candidates scanned by K2 (sum over queries) */
+    int64_t alpha4_queries;  /* queries on the exact alpha = 4 recipe  */
+    int64_t kernel_launches; /* kernels launched by this call          */
+} aidw_run_stats;
+
+/* ------------------------------------------------------------ info */
+int aidw_capi_version(void);
+/* Number of kernels this library has launched since load (all threads). */
+int64_t aidw_kernel_launch_count(void);
+/* Device name / SM count of the current device; fails without CUDA. */
+int aidw_device_info(char* name, size_t cap, int32_t* sm_count, aidw_error* err);
+void aidw_set_weight_precision(int32_t precision);
+int32_t aidw_get_weight_precision(void);
+/* 1 (default): queries with alpha == 4 exactly take the one-MUFU recipe
+ * w = 1/(d2*d2) (the reference's half-integer recipe, interpolate.hpp:
+ * 174-209); 0: every query takes the general exp2/log2 path (used to report
+ * the general-alpha roofline separately). */
+void aidw_set_alpha4_recipe(int32_t enabled);
+
+/* ------------------------------------------------------------ grid (K1) */
+/* build_index — grid.hpp:176-213.  sorted_ids/sorted_x/sorted_y: m entries,
+ * cell_start: n_col*n_row + 1 entries (exclusive prefix). */
+int aidw_build_index(const double* xs, const double* ys, size_t m, const aidw_grid_config* cfg,
+                     uint32_t* sorted_ids, uint32_t* cell_start, double* sorted_x,
+                     double* sorted_y, aidw_error* err);
+
+/* ------------------------------------------------------------ kNN (K2) */
+/* knn_stage — knn.hpp:255-271.  Grid engine: pass the GridIndex arrays from
+ * build_index (cfg, cell_start, sorted_ids, sorted_x, sorted_y); brute
+ * engine: they may be NULL.  Outputs (k_eff = min(k, m) for the grid
+ * engine; brute requires k <= m):
+ *   d2_out   n * k_eff squared distances, ascending (KnnResult::distances_sq)
+ *   idx_out  n * k_eff data indices, (d2, idx)-lexicographic (nullable)
+ *   avg_out  n  KnnResult::average_distance
+ *   *k_eff_out, *exhausted_out (KnnResult::exhausted, same for all queries) */
+int aidw_knn_stage(const double* qx, const double* qy, size_t n, const aidw_grid_config* cfg,
+                   const uint32_t* cell_start, const uint32_t* sorted_ids,
+                   const double* sorted_x, const double* sorted_y, const double* dx,
+                   const double* dy, size_t m, int32_t k, int32_t engine, double* d2_out,
+                   uint32_t* idx_out, double* avg_out, int32_t* k_eff_out,
+                   int32_t* exhausted_out, aidw_error* err);
+
+/* ------------------------------------------------------------ weighting (K3+K4) */
+/* aidw_predict_all — interpolate.hpp:453-489.  Per query i the caller's
+ * KnnResult is summarised as r_obs[i] (average_distance), list_len[i]
+ * (size()) and exhausted[i]. */
+int aidw_aidw_predict_all(const double* qx, const double* qy, size_t n, const double* dx,
+                          const double* dy, const double* dz, size_t m, const double* r_obs,
+                          const int64_t* list_len, const uint8_t* exhausted,
+                          const aidw_params* params, int32_t variant, int32_t pinned_order,
+                          double* pred_out, double* alpha_out, aidw_error* err);
+
+/* idw_predict_all — interpolate.hpp:426-448 (constant alpha). */
+int aidw_idw_predict_all(const double* qx, const double* qy, size_t n, const double* dx,
+                         const double* dy, const double* dz, size_t m, double alpha,
+                         int32_t variant, int32_t pinned_order, double* pred_out,
+                         double* alpha_out, aidw_error* err);
+
+/* ------------------------------------------------------------ pipeline */
+/* cli::run_pipeline — cli.hpp:217-268, fused and device-resident between
+ * stages (no per-query KnnResult materialisation).  Host buffers. */
+int aidw_run_pipeline(const double* dx, const double* dy, const double* dz, size_t m,
+                      const double* qx, const double* qy, size_t n, const aidw_run_config* cfg,
+                      double* pred_out, double* alpha_out, aidw_run_stats* stats,
+                      aidw_error* err);
+
+/* Same pipeline over DEVICE-resident inputs/outputs (current device).
+ * `stream` is a cudaStream_t (NULL = the library's own stream). */
+int aidw_run_pipeline_device(const double* d_dx, const double* d_dy, const double* d_dz,
+                             size_t m, const double* d_qx, const double* d_qy, size_t n,
+                             const aidw_run_config* cfg, double* d_pred, double* d_alpha,
+                             aidw_run_stats* stats, void* stream, aidw_error* err);
+
+/* bbox(data ∪ queries) of device-resident sets (types.hpp:124-143);
+ * out = {min_x, min_y, max_x, max_y}.  For sharded runs: all-reduce MIN/MAX
+ * of the per-rank boxes, then pass the result as aidw_run_config.bbox. */
+int aidw_compute_bbox_device(const double* d_dx, const double* d_dy, size_t m,
+                             const double* d_qx, const double* d_qy, size_t n, double* out,
+                             void* stream, aidw_error* err);
+
+/* ------------------------------------------------------------ synthetic inputs */
+/* generate_random_points / generate_random_queries — generate.hpp:45-95
+ * (mt19937_64, 53-bit unit doubles; rule 0 uniform, 1 planar, 2 radial). */
+int aidw_generate_points(size_t count, const double* bbox, uint64_t seed, int32_t rule,
+                         double* xs, double* ys, double* zs, aidw_error* err);
+int aidw_generate_queries(size_t count, const double* bbox, uint64_t seed, double* xs,
+                          double* ys, aidw_error* err);
+/* Clustered (Gaussian-blob) points for BASELINE config 4 (the
+ * reference has no such generator).  zs may be NULL for query sets. */
+int aidw_generate_clustered(size_t count, int32_t blobs, double sigma, uint64_t center_seed,
+                            uint64_t seed, double* xs, double* ys, double* zs, aidw_error* err);
+/* cmd_raster lattice (cli.hpp:496-507): nx*ny cell centres over bbox,
+ * northernmost row first, row-major. */
+int aidw_raster_lattice(size_t nx, size_t ny, const double* bbox, double* xs, double* ys,
+                        aidw_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AIDW_CAPI_H */

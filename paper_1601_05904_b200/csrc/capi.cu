@@ -1,0 +1,868 @@
+// capi.cu — the extern "C" entry points (include/aidw_capi.h) and the fused,
+// device-resident run_pipeline.
+//
+// Host code here only validates, computes the reference's scalar set-up
+// (cell width, grid geometry, r_exp, snap tolerance — with the reference's
+// own expressions, compiled with -ffp-contract=off) and orchestrates the
+// sm_100a kernels of grid_build.cu (K1), knn.cu (K2 + K3) and weight.cu /
+// weight64.cu (K4).  No per-query arithmetic of the hot path runs on the
+// host; without a CUDA device every entry point fails with AIDW_ERR_CUDA.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <new>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "aidw_capi.h"
+#include "common.cuh"
+#include "knn.cuh"
+#include "weight.cuh"
+
+namespace aidwb {
+
+std::atomic<long long> g_launches{0};
+
+namespace {
+
+std::atomic<int> g_precision{[] {
+    const char* e = std::getenv("AIDW_WEIGHT_FP64");
+    return (e && e[0] == '1') ? AIDW_PRECISION_FP64 : AIDW_PRECISION_FP32;
+}()};
+
+// ------------------------------------------------------------ host set-up
+// The reference's scalar expressions (types.hpp, grid.hpp, adaptive.hpp,
+// interpolate.hpp), evaluated on the host exactly as written there.
+struct Box {
+    double min_x, min_y, max_x, max_y;
+    double width() const { return max_x - min_x; }
+    double height() const { return max_y - min_y; }
+    double area() const { return width() * height(); }
+    bool valid() const { return min_x <= max_x && min_y <= max_y; }
+    bool degenerate() const { return !(area() > 0.0); }
+};
+
+double choose_cell_width_h(size_t m, const Box& b, double factor) {  // grid.hpp:50-64
+    if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "choose_cell_width: data set is empty");
+    if (!b.valid() || b.degenerate())
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "choose_cell_width: bbox must have positive area");
+    if (!(factor > 0.0) || !std::isfinite(factor))
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "choose_cell_width: factor must be positive finite");
+    const double density = static_cast<double>(m) / b.area();
+    return factor * (1.0 / (2.0 * std::sqrt(density)));
+}
+
+aidw_grid_config make_grid_config_h(const Box& b, double w) {  // grid.hpp:67-88
+    if (!b.valid() || b.degenerate())
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "make_grid_config: bbox must have positive area");
+    if (!(w > 0.0) || !std::isfinite(w))
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "make_grid_config: cellWidth must be positive finite");
+    const double cols = std::floor((b.max_x - b.min_x + w) / w);
+    const double rows = std::floor((b.max_y - b.min_y + w) / w);
+    if (cols * rows > 1.0e9)
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT,
+                      "make_grid_config: cellWidth " + std::to_string(w) + " yields more than 1e9 cells");
+    aidw_grid_config c;
+    c.cell_width = w;
+    c.n_col = std::max(1, static_cast<int>(cols));
+    c.n_row = std::max(1, static_cast<int>(rows));
+    c.min_x = b.min_x;
+    c.min_y = b.min_y;
+    return c;
+}
+
+void validate_params(const aidw_params& p) {  // types.hpp:102-114
+    if (p.k < 1)
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "AidwParams: k must be >= 1, got " + std::to_string(p.k));
+    if (!(p.r_min < p.r_max)) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "AidwParams: rMin must be < rMax");
+    for (double a : p.alpha_levels)
+        if (!(a > 0.0) || !std::isfinite(a))
+            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "AidwParams: alpha levels must be positive finite");
+}
+
+AlphaParams alpha_params_h(const aidw_params& p, double r_exp) {
+    AlphaParams a;
+    a.r_exp = r_exp;
+    a.pi_over_rmax = std::numbers::pi / p.r_max;  // adaptive.hpp:59
+    a.r_min = p.r_min;
+    a.r_max = p.r_max;
+    for (int i = 0; i < 5; ++i) a.lv[i] = p.alpha_levels[i];
+    return a;
+}
+
+double snap_sq_h(const Box& b) {  // interpolate.hpp:86-89
+    const double eps = 1.0e-12 * std::hypot(b.width(), b.height());
+    return eps * eps;
+}
+
+WeightFrame make_frame(const Box& b, double zlo, double zhi) {
+    WeightFrame f;
+    f.ox = b.min_x;
+    f.oy = b.min_y;
+    const double span = std::max(b.width(), b.height());
+    f.inv_scale = (span > 0.0 && std::isfinite(span)) ? 1.0 / span : 1.0;
+    const double zmax = std::max(std::fabs(zlo), std::fabs(zhi));
+    int e = 0;
+    if (zmax > 0.0 && std::isfinite(zmax)) std::frexp(zmax, &e);
+    f.zshift = -e;  // |z * 2^zshift| < 1
+    f.zlo = zlo;
+    f.zhi = zhi;
+    f.snap_sq = snap_sq_h(b);
+    return f;
+}
+
+std::string locate_msg(double x, double y) {  // grid.hpp:100-101
+    return "locate_cell: point (" + std::to_string(x) + ", " + std::to_string(y) +
+           ") lies outside the covered region";
+}
+
+// ------------------------------------------------------------ device context
+std::once_flag g_pool_once[64];
+
+int current_device() {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw Failure(AIDW_ERR_CUDA, std::string("no CUDA device available: ") +
+                                          (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::call_once(g_pool_once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = std::numeric_limits<uint64_t>::max();
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    return dev;
+}
+
+struct StreamScope {
+    cudaStream_t s = nullptr;
+    bool own = false;
+    explicit StreamScope(void* external = nullptr) {
+        current_device();
+        if (external) {
+            s = static_cast<cudaStream_t>(external);
+        } else {
+            CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            own = true;
+        }
+    }
+    void sync() { CK(cudaStreamSynchronize(s)); }
+    ~StreamScope() {
+        if (own) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t make() {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ev.push_back(e);
+        return e;
+    }
+    static double ms(cudaEvent_t a, cudaEvent_t b) {
+        float t = 0.f;
+        if (a && b && cudaEventElapsedTime(&t, a, b) == cudaSuccess) return t;
+        return 0.0;
+    }
+    ~Events() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+template <typename T>
+void h2d(DBuf<T>& dst, const T* src, size_t n, cudaStream_t s) {
+    dst.alloc(n, s);
+    if (n) CK(cudaMemcpyAsync(dst.get(), src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+template <typename T>
+void d2h(T* dst, const T* src, size_t n, cudaStream_t s) {
+    if (n && dst) CK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+// bbox of (a ∪ b) plus the z hull, device reduce -> host.
+struct Extents {
+    Box box;
+    double zlo, zhi;
+};
+Extents extents(const double* ax, const double* ay, size_t na, const double* bx, const double* by,
+                size_t nb, const double* z, size_t nz, cudaStream_t s) {
+    DBuf<double> out(6, s);
+    bbox_reduce_device(ax, ay, na, bx, by, nb, z, nz, out.get(), s);
+    double h[6];
+    d2h(h, out.get(), 6, s);
+    CK(cudaStreamSynchronize(s));
+    return Extents{Box{h[0], h[1], h[2], h[3]}, h[4], h[5]};
+}
+
+// Failure indices written by kernels (atomicMin), resolved after sync.
+struct FailFlags {
+    DBuf<long long> d;
+    long long h[4];
+    explicit FailFlags(cudaStream_t s) : d(4, s) {
+        const long long init[4] = {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MAX};
+        std::memcpy(h, init, sizeof h);
+        CK(cudaMemcpyAsync(d.get(), h, sizeof h, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // h is reused as the D2H target
+    }
+    long long* slot(int i) { return d.get() + i; }
+    void fetch(cudaStream_t s) {
+        d2h(h, d.get(), 4, s);
+        CK(cudaStreamSynchronize(s));
+    }
+};
+enum { kFailData = 0, kFailQuery = 1, kFailAlpha = 2 };
+
+// Device-side nearest / snap search for the weighting stage when no kNN
+// stage ran (idw mode and the aidw_predict_all drop-in).  Uses a k = 1 grid
+// search (K1 + K2), or the brute kernel for tiny / degenerate sets.
+struct NearestInfo {
+    DBuf<uint32_t> perm;  // visiting order
+    DBuf<double> d2min;
+    DBuf<uint32_t> nn, snap;
+};
+
+void nearest_search(const double* d_dx, const double* d_dy, size_t m, const double* d_qx,
+                    const double* d_qy, size_t n, const Box& box, double snap_sq,
+                    NearestInfo& out, FailFlags& fails, cudaStream_t s) {
+    out.d2min.alloc(n, s);
+    out.nn.alloc(n, s);
+    out.snap.alloc(n, s);
+    KnnArgs a;
+    a.qx = d_qx;
+    a.qy = d_qy;
+    a.n = n;
+    a.m = m;
+    a.k = 1;
+    a.k_eff = 1;
+    a.snap_sq = snap_sq;
+    a.d2min_s = out.d2min.get();
+    a.nn_s = out.nn.get();
+    a.snap_s = out.snap.get();
+    bool use_grid = m > 4096 && box.valid() && !box.degenerate() && std::isfinite(box.area());
+    aidw_grid_config cfg{};
+    if (use_grid) {
+        try {
+            cfg = make_grid_config_h(box, choose_cell_width_h(m, box, 4.0));
+        } catch (const Failure&) {
+            use_grid = false;
+        }
+    }
+    if (!use_grid) {
+        out.perm.alloc(0, s);
+        a.dx = d_dx;
+        a.dy = d_dy;
+        run_knn_brute(a, s);
+        return;
+    }
+    DeviceGrid g;
+    build_grid_device(d_dx, d_dy, m, cfg, g, fails.slot(kFailData), s);
+    DBuf<uint32_t> qcell;
+    const GridGeom geom = make_geom(cfg);
+    sort_queries_by_cell(d_qx, d_qy, n, geom, out.perm, qcell, fails.slot(kFailQuery), s);
+    a.g = geom;
+    a.cell_start = g.cell_start.get();
+    a.sorted_ids = g.sorted_ids.get();
+    a.sorted_x = g.sorted_x.get();
+    a.sorted_y = g.sorted_y.get();
+    a.perm = out.perm.get();
+    a.qcell = qcell.get();
+    run_knn_grid(a, s);
+}
+
+// Device "alpha by visiting position" = gather of alpha-by-query.
+__global__ void gather_f64_kernel(const double* __restrict__ src, const uint32_t* __restrict__ perm,
+                                  size_t n, double* __restrict__ dst) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[perm ? perm[i] : i];
+}
+__global__ void fill_f64_kernel(double* __restrict__ dst, size_t n, double v) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = v;
+}
+
+bool use_fp64(int32_t variant, int32_t pinned) {
+    return variant == AIDW_VARIANT_NAIVE || pinned != 0 ||
+           g_precision.load(std::memory_order_relaxed) == AIDW_PRECISION_FP64;
+}
+
+// Weighting stage over device-resident inputs given alpha by query index.
+// d_alpha_q: alpha per query (input order).
+void weighting_stage(const double* d_dx, const double* d_dy, const double* d_dz, size_t m,
+                     const double* d_qx, const double* d_qy, size_t n, const double* d_alpha_q,
+                     const Extents& ext, bool fp64, double* d_pred, double* d_alpha_out,
+                     FailFlags& fails, WeightTimes* wt, cudaStream_t s) {
+    const WeightFrame frame = make_frame(ext.box, ext.zlo, ext.zhi);
+    WeightData wd{d_dx, d_dy, d_dz, m};
+    if (fp64) {
+        WeightQueries q;
+        q.qx = d_qx;
+        q.qy = d_qy;
+        q.n = n;
+        q.alpha_s = d_alpha_q;
+        weighting_fp64(q, wd, frame, d_pred, d_alpha_out, wt, s);
+        return;
+    }
+    NearestInfo nb;
+    nearest_search(d_dx, d_dy, m, d_qx, d_qy, n, ext.box, frame.snap_sq, nb, fails, s);
+    const uint32_t* perm = nb.perm.n ? nb.perm.get() : nullptr;
+    DBuf<double> alpha_s(n, s);
+    LAUNCH(gather_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_alpha_q, perm, n,
+           alpha_s.get());
+    WeightQueries q;
+    q.qx = d_qx;
+    q.qy = d_qy;
+    q.n = n;
+    q.perm = perm;
+    q.alpha_s = alpha_s.get();
+    q.d2min_s = nb.d2min.get();
+    q.nn_s = nb.nn.get();
+    q.snap_s = nb.snap.get();
+    weighting_fp32(q, wd, frame, d_pred, d_alpha_out, wt, s);
+}
+
+void fill_error(aidw_error* err, int code, const std::string& msg, long long index) {
+    if (!err) return;
+    err->code = code;
+    err->index = index;
+    std::strncpy(err->message, msg.c_str(), sizeof(err->message) - 1);
+    err->message[sizeof(err->message) - 1] = '\0';
+}
+
+template <class F>
+int guarded(aidw_error* err, F&& body) {
+    if (err) fill_error(err, AIDW_OK, "", -1);
+    try {
+        body();
+        return AIDW_OK;
+    } catch (const Failure& f) {
+        fill_error(err, f.code, f.msg, f.index);
+        return f.code;
+    } catch (const std::bad_alloc&) {
+        fill_error(err, AIDW_ERR_RUNTIME, "host allocation failed", -1);
+        return AIDW_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        fill_error(err, AIDW_ERR_RUNTIME, e.what(), -1);
+        return AIDW_ERR_RUNTIME;
+    }
+}
+
+// ------------------------------------------------------------ pipeline core
+struct PipelineIO {
+    const double *dx, *dy, *dz, *qx, *qy;  // device
+    size_t m, n;
+    double *pred, *alpha;                  // device
+};
+
+// The fused run_pipeline (cli.hpp:217-268) over device-resident buffers.
+void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_stats* st,
+                   Events& ev, cudaStream_t s, std::vector<cudaEvent_t>& marks,
+                   cudaEvent_t& k4b, cudaEvent_t& k4e, cudaEvent_t& knnb, cudaEvent_t& knne,
+                   unsigned long long*& d_a4, DBuf<unsigned long long>& a4buf,
+                   DBuf<unsigned long long>& candbuf) {
+    if (cfg.workers < 0)
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "resolve_workers: worker count must be >= 0");
+    const size_t m = io.m, n = io.n;
+    if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set is empty");
+    if (!io.dz) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set carries no values");
+    FailFlags fails(s);
+    a4buf.alloc(1, s);
+    candbuf.alloc(1, s);
+    CK(cudaMemsetAsync(a4buf.get(), 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(candbuf.get(), 0, sizeof(unsigned long long), s));
+    d_a4 = a4buf.get();
+    const bool fp64 = use_fp64(cfg.variant, 0);
+    WeightTimes wt;
+    wt.k4_begin = k4b = ev.make();
+    wt.k4_end = k4e = ev.make();
+    wt.d_alpha4 = d_a4;
+
+    // bbox(data ∪ queries) and the value hull
+    Extents ext;
+    if (cfg.use_bbox) {
+        ext = extents(nullptr, nullptr, 0, nullptr, nullptr, 0, io.dz, m, s);
+        ext.box = Box{cfg.bbox[0], cfg.bbox[1], cfg.bbox[2], cfg.bbox[3]};
+    } else {
+        ext = extents(io.dx, io.dy, m, io.qx, io.qy, n, io.dz, m, s);
+    }
+    const cudaEvent_t e_build0 = ev.make(), e_build1 = ev.make(), e_knn1 = ev.make(),
+                      e_interp1 = ev.make();
+    marks = {e_build0, e_build1, e_knn1, e_interp1};
+
+    if (cfg.mode == AIDW_MODE_IDW) {
+        if (!(cfg.alpha > 0.0) || !std::isfinite(cfg.alpha))
+            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "idw_predict_all: alpha must be positive finite");
+        CK(cudaEventRecord(e_build0, s));
+        CK(cudaEventRecord(e_build1, s));
+        CK(cudaEventRecord(e_knn1, s));
+        DBuf<double> alpha_q(n, s);
+        if (n) LAUNCH(fill_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, alpha_q.get(), n, cfg.alpha);
+        weighting_stage(io.dx, io.dy, io.dz, m, io.qx, io.qy, n, alpha_q.get(), ext, fp64,
+                        io.pred, io.alpha, fails, &wt, s);
+        CK(cudaEventRecord(e_interp1, s));
+        fails.fetch(s);
+        if (st) st->k_effective = 0;
+        return;
+    }
+
+    // k clamp (cli.hpp:237-238): the reference converts k to size_t first,
+    // so a negative k clamps to m as well.
+    aidw_params params = cfg.params;
+    params.k = static_cast<int32_t>(
+        std::min<size_t>(static_cast<size_t>(static_cast<int64_t>(cfg.params.k)), m));
+    if (st) st->k_effective = params.k;
+    const int k = params.k;
+
+    KnnArgs a;
+    a.qx = io.qx;
+    a.qy = io.qy;
+    a.n = n;
+    a.m = m;
+    a.k = k;
+    a.k_eff = k;
+    a.candidates = candbuf.get();
+    const double area = params.area > 0.0 ? params.area : ext.box.area();
+    const double r_exp_arg = static_cast<double>(m) / area;
+    if (!(area > 0.0) || !std::isfinite(area))
+        throw Failure(AIDW_ERR_RUNTIME,
+                      "aidw_predict_all: query 0: expected_nn_distance: area must be positive finite", 0);
+    const double r_exp = 1.0 / (2.0 * std::sqrt(r_exp_arg));  // adaptive.hpp:27
+    const WeightFrame frame = make_frame(ext.box, ext.zlo, ext.zhi);
+    a.snap_sq = frame.snap_sq;
+    a.compute_alpha = 1;
+    a.ap = alpha_params_h(params, r_exp);
+    a.fail_alpha = fails.slot(kFailAlpha);
+
+    DBuf<double> alpha_s(n, s), d2min_s(n, s);
+    DBuf<uint32_t> nn_s(n, s), snap_s(n, s), perm, qcell;
+    a.alpha_s = alpha_s.get();
+    a.d2min_s = d2min_s.get();
+    a.nn_s = nn_s.get();
+    a.snap_s = snap_s.get();
+    knnb = ev.make();
+    knne = ev.make();
+
+    if (cfg.engine == AIDW_ENGINE_GRID) {
+        const double width = choose_cell_width_h(m, ext.box, cfg.cell_factor);
+        const aidw_grid_config gc = make_grid_config_h(ext.box, width);
+        validate_params(params);
+        CK(cudaEventRecord(e_build0, s));
+        DeviceGrid g;
+        build_grid_device(io.dx, io.dy, m, gc, g, fails.slot(kFailData), s);
+        CK(cudaEventRecord(e_build1, s));
+        const GridGeom geom = make_geom(gc);
+        sort_queries_by_cell(io.qx, io.qy, n, geom, perm, qcell, fails.slot(kFailQuery), s);
+        a.g = geom;
+        a.cell_start = g.cell_start.get();
+        a.sorted_ids = g.sorted_ids.get();
+        a.sorted_x = g.sorted_x.get();
+        a.sorted_y = g.sorted_y.get();
+        a.perm = perm.get();
+        a.qcell = qcell.get();
+        CK(cudaEventRecord(knnb, s));
+        run_knn_grid(a, s);
+        CK(cudaEventRecord(knne, s));
+        CK(cudaEventRecord(e_knn1, s));
+    } else {
+        validate_params(params);
+        CK(cudaEventRecord(e_build0, s));
+        CK(cudaEventRecord(e_build1, s));
+        a.dx = io.dx;
+        a.dy = io.dy;
+        CK(cudaEventRecord(knnb, s));
+        run_knn_brute(a, s);
+        CK(cudaEventRecord(knne, s));
+        CK(cudaEventRecord(e_knn1, s));
+    }
+
+    WeightData wd{io.dx, io.dy, io.dz, m};
+    WeightQueries q;
+    q.qx = io.qx;
+    q.qy = io.qy;
+    q.n = n;
+    q.perm = perm.n ? perm.get() : nullptr;
+    q.alpha_s = alpha_s.get();
+    q.d2min_s = d2min_s.get();
+    q.nn_s = nn_s.get();
+    q.snap_s = snap_s.get();
+    if (fp64)
+        weighting_fp64(q, wd, frame, io.pred, io.alpha, &wt, s);
+    else
+        weighting_fp32(q, wd, frame, io.pred, io.alpha, &wt, s);
+    CK(cudaEventRecord(e_interp1, s));
+    fails.fetch(s);
+    if (fails.h[kFailQuery] != LLONG_MAX)
+        throw Failure(AIDW_ERR_RUNTIME,
+                      "knn_stage: query " + std::to_string(fails.h[kFailQuery]) +
+                          ": locate_cell: point lies outside the covered region",
+                      fails.h[kFailQuery]);
+    if (fails.h[kFailData] != LLONG_MAX)
+        throw Failure(AIDW_ERR_DOMAIN, "locate_cell: data point " + std::to_string(fails.h[kFailData]) +
+                                           " lies outside the covered region",
+                      fails.h[kFailData]);
+    if (fails.h[kFailAlpha] != LLONG_MAX)
+        throw Failure(AIDW_ERR_RUNTIME,
+                      "aidw_predict_all: query " + std::to_string(fails.h[kFailAlpha]) +
+                          ": alpha_from_mu: mu outside [0, 1]",
+                      fails.h[kFailAlpha]);
+}
+
+void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_stats* st,
+                    cudaStream_t s, double h2d_ms, const std::chrono::steady_clock::time_point& t0,
+                    double* h_pred, double* h_alpha) {
+    const long long launches0 = g_launches.load();
+    Events ev;
+    std::vector<cudaEvent_t> marks;
+    cudaEvent_t k4b = nullptr, k4e = nullptr, knnb = nullptr, knne = nullptr;
+    unsigned long long* d_a4 = nullptr;
+    DBuf<unsigned long long> a4buf, candbuf;
+    aidw_run_stats local{};
+    pipeline_core(io, cfg, &local, ev, s, marks, k4b, k4e, knnb, knne, d_a4, a4buf, candbuf);
+    double d2h_ms = 0.0;
+    if (h_pred) {
+        const auto c0 = std::chrono::steady_clock::now();
+        d2h(h_pred, io.pred, io.n, s);
+        if (h_alpha) d2h(h_alpha, io.alpha, io.n, s);
+        CK(cudaStreamSynchronize(s));
+        d2h_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+    }
+    CK(cudaStreamSynchronize(s));
+    if (st) {
+        *st = local;
+        st->build_ms = Events::ms(marks[0], marks[1]);
+        st->knn_ms = Events::ms(marks[1], marks[2]);
+        st->interp_ms = Events::ms(marks[2], marks[3]);
+        st->weight_kernel_ms = Events::ms(k4b, k4e);
+        st->knn_kernel_ms = Events::ms(knnb, knne);
+        st->h2d_ms = h2d_ms;
+        st->d2h_ms = d2h_ms;
+        st->worker_count = cfg.workers > 0 ? cfg.workers : 1;
+        st->pairs = static_cast<int64_t>(io.m) * static_cast<int64_t>(io.n);
+        unsigned long long h = 0;
+        if (a4buf.get()) CK(cudaMemcpy(&h, a4buf.get(), sizeof h, cudaMemcpyDeviceToHost));
+        st->alpha4_queries = static_cast<int64_t>(h);
+        h = 0;
+        if (candbuf.get()) CK(cudaMemcpy(&h, candbuf.get(), sizeof h, cudaMemcpyDeviceToHost));
+        st->knn_candidates = static_cast<int64_t>(h);
+        st->kernel_launches = g_launches.load() - launches0;
+        st->total_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+}
+
+}  // namespace
+}  // namespace aidwb
+
+using namespace aidwb;
+
+extern "C" {
+
+int aidw_capi_version(void) { return AIDW_CAPI_VERSION; }
+
+int64_t aidw_kernel_launch_count(void) { return g_launches.load(); }
+
+void aidw_set_weight_precision(int32_t precision) {
+    g_precision.store(precision == AIDW_PRECISION_FP64 ? AIDW_PRECISION_FP64 : AIDW_PRECISION_FP32);
+}
+
+int32_t aidw_get_weight_precision(void) { return g_precision.load(); }
+
+void aidw_set_alpha4_recipe(int32_t enabled) { set_alpha4_recipe(enabled != 0); }
+
+int aidw_device_info(char* name, size_t cap, int32_t* sm_count, aidw_error* err) {
+    return guarded(err, [&] {
+        const int dev = current_device();
+        cudaDeviceProp p;
+        CK(cudaGetDeviceProperties(&p, dev));
+        if (name && cap) {
+            std::strncpy(name, p.name, cap - 1);
+            name[cap - 1] = '\0';
+        }
+        if (sm_count) *sm_count = p.multiProcessorCount;
+    });
+}
+
+int aidw_build_index(const double* xs, const double* ys, size_t m, const aidw_grid_config* cfg,
+                     uint32_t* sorted_ids, uint32_t* cell_start, double* sorted_x,
+                     double* sorted_y, aidw_error* err) {
+    return guarded(err, [&] {
+        if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: data set is empty");
+        if (m > static_cast<size_t>(std::numeric_limits<uint32_t>::max()) - 1)
+            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: too many points for 32-bit ids");
+        if (!cfg || cfg->n_col < 1 || cfg->n_row < 1 || !(cfg->cell_width > 0.0))
+            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: invalid grid configuration");
+        StreamScope ss;
+        cudaStream_t s = ss.s;
+        FailFlags fails(s);
+        DBuf<double> dx, dy;
+        h2d(dx, xs, m, s);
+        h2d(dy, ys, m, s);
+        DeviceGrid g;
+        build_grid_device(dx.get(), dy.get(), m, *cfg, g, fails.slot(kFailData), s);
+        fails.fetch(s);
+        if (fails.h[kFailData] != LLONG_MAX) {
+            const long long i = fails.h[kFailData];
+            throw Failure(AIDW_ERR_DOMAIN, locate_msg(xs[i], ys[i]), i);
+        }
+        d2h(sorted_ids, g.sorted_ids.get(), m, s);
+        d2h(cell_start, g.cell_start.get(), g.cells + 1, s);
+        d2h(sorted_x, g.sorted_x.get(), m, s);
+        d2h(sorted_y, g.sorted_y.get(), m, s);
+        ss.sync();
+    });
+}
+
+int aidw_knn_stage(const double* qx, const double* qy, size_t n, const aidw_grid_config* cfg,
+                   const uint32_t* cell_start, const uint32_t* sorted_ids,
+                   const double* sorted_x, const double* sorted_y, const double* dx,
+                   const double* dy, size_t m, int32_t k, int32_t engine, double* d2_out,
+                   uint32_t* idx_out, double* avg_out, int32_t* k_eff_out,
+                   int32_t* exhausted_out, aidw_error* err) {
+    return guarded(err, [&] {
+        const bool grid = engine == AIDW_ENGINE_GRID;
+        if (grid && (!cfg || !cell_start || (m > 0 && (!sorted_ids || !sorted_x || !sorted_y))))
+            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "knn_stage: grid engine requires a grid index");
+        int k_eff = grid ? static_cast<int>(std::min<int64_t>(k, static_cast<int64_t>(m))) : k;
+        const bool exhausted = grid && static_cast<int64_t>(m) < k;
+        if (k_eff_out) *k_eff_out = k_eff;
+        if (exhausted_out) *exhausted_out = exhausted ? 1 : 0;
+        if (n == 0) return;
+        if (grid) {
+            if (m == 0) throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: grid_knn: index holds no points", 0);
+            if (k < 1) throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: grid_knn: k must be >= 1", 0);
+        } else {
+            if (m == 0)
+                throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: brute_force_knn: data set is empty", 0);
+            if (k < 1 || static_cast<size_t>(k) > m)
+                throw Failure(AIDW_ERR_RUNTIME,
+                              "knn_stage: query 0: brute_force_knn: k = " + std::to_string(k) +
+                                  " outside [1, " + std::to_string(m) + "]", 0);
+        }
+        StreamScope ss;
+        cudaStream_t s = ss.s;
+        FailFlags fails(s);
+        DBuf<double> dqx, dqy, d2(n * static_cast<size_t>(k_eff), s), avg(n, s);
+        DBuf<uint32_t> ids(idx_out ? n * static_cast<size_t>(k_eff) : 0, s);
+        h2d(dqx, qx, n, s);
+        h2d(dqy, qy, n, s);
+        KnnArgs a;
+        a.qx = dqx.get();
+        a.qy = dqy.get();
+        a.n = n;
+        a.m = m;
+        a.k = k;
+        a.k_eff = k_eff;
+        a.d2_out = d2.get();
+        a.id_out = idx_out ? ids.get() : nullptr;
+        a.avg_out = avg.get();
+        DBuf<double> ddx, ddy, sx, sy;
+        DBuf<uint32_t> cs, sid, perm, qcell;
+        if (grid) {
+            const size_t cells = static_cast<size_t>(cfg->n_col) * static_cast<size_t>(cfg->n_row);
+            h2d(cs, cell_start, cells + 1, s);
+            h2d(sid, sorted_ids, m, s);
+            h2d(sx, sorted_x, m, s);
+            h2d(sy, sorted_y, m, s);
+            const GridGeom geom = make_geom(*cfg);
+            sort_queries_by_cell(dqx.get(), dqy.get(), n, geom, perm, qcell, fails.slot(kFailQuery), s);
+            fails.fetch(s);
+            if (fails.h[kFailQuery] != LLONG_MAX) {
+                const long long i = fails.h[kFailQuery];
+                throw Failure(AIDW_ERR_RUNTIME,
+                              "knn_stage: query " + std::to_string(i) + ": " + locate_msg(qx[i], qy[i]), i);
+            }
+            a.g = geom;
+            a.cell_start = cs.get();
+            a.sorted_ids = sid.get();
+            a.sorted_x = sx.get();
+            a.sorted_y = sy.get();
+            a.perm = perm.get();
+            a.qcell = qcell.get();
+            run_knn_grid(a, s);
+        } else {
+            h2d(ddx, dx, m, s);
+            h2d(ddy, dy, m, s);
+            a.dx = ddx.get();
+            a.dy = ddy.get();
+            run_knn_brute(a, s);
+        }
+        d2h(d2_out, d2.get(), n * static_cast<size_t>(k_eff), s);
+        if (idx_out) d2h(idx_out, ids.get(), n * static_cast<size_t>(k_eff), s);
+        d2h(avg_out, avg.get(), n, s);
+        ss.sync();
+    });
+}
+
+int aidw_aidw_predict_all(const double* qx, const double* qy, size_t n, const double* dx,
+                          const double* dy, const double* dz, size_t m, const double* r_obs,
+                          const int64_t* list_len, const uint8_t* exhausted,
+                          const aidw_params* params, int32_t variant, int32_t pinned_order,
+                          double* pred_out, double* alpha_out, aidw_error* err) {
+    return guarded(err, [&] {
+        if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set is empty");
+        if (!dz) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set carries no values");
+        if (!params) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "aidw_predict_all: params missing");
+        validate_params(*params);
+        if (n == 0) return;
+        StreamScope ss;
+        cudaStream_t s = ss.s;
+        FailFlags fails(s);
+        DBuf<double> ddx, ddy, ddz, dqx, dqy, drobs, alpha_q(n, s), pred(n, s), alpha_o(n, s);
+        h2d(ddx, dx, m, s);
+        h2d(ddy, dy, m, s);
+        h2d(ddz, dz, m, s);
+        h2d(dqx, qx, n, s);
+        h2d(dqy, qy, n, s);
+        h2d(drobs, r_obs, n, s);
+        const Extents ext = extents(ddx.get(), ddy.get(), m, dqx.get(), dqy.get(), n, ddz.get(), m, s);
+        const double area = params->area > 0.0 ? params->area : ext.box.area();
+        // adaptive_alpha's host-checkable preconditions, first failing query
+        // (adaptive.hpp:101-112): size, area, r_exp, r_obs sign.
+        const bool area_ok = area > 0.0 && std::isfinite(area);
+        const double r_exp = area_ok ? 1.0 / (2.0 * std::sqrt(static_cast<double>(m) / area)) : 0.0;
+        long long host_fail = -1;
+        std::string host_msg;
+        for (size_t i = 0; i < n && host_fail < 0; ++i) {
+            const bool exh = exhausted && exhausted[i];
+            if (!exh && list_len && list_len[i] != params->k) {
+                host_fail = static_cast<long long>(i);
+                host_msg = "adaptive_alpha: kNN result holds " + std::to_string(list_len[i]) +
+                           " distances, expected " + std::to_string(params->k);
+            } else if (!area_ok) {
+                host_fail = static_cast<long long>(i);
+                host_msg = "expected_nn_distance: area must be positive finite";
+            } else if (!(r_exp > 0.0)) {
+                host_fail = static_cast<long long>(i);
+                host_msg = "nn_statistic: rExp must be positive";
+            } else if (r_obs[i] < 0.0) {
+                host_fail = static_cast<long long>(i);
+                host_msg = "nn_statistic: rObs must be non-negative";
+            }
+        }
+        const AlphaParams ap = alpha_params_h(*params, r_exp > 0.0 ? r_exp : 1.0);
+        run_alpha(drobs.get(), n, ap, alpha_q.get(), fails.slot(kFailAlpha), s);
+        fails.fetch(s);
+        const long long dev_fail = fails.h[kFailAlpha] == LLONG_MAX ? -1 : fails.h[kFailAlpha];
+        if (host_fail >= 0 || dev_fail >= 0) {
+            long long i = host_fail;
+            std::string msg = host_msg;
+            if (i < 0 || (dev_fail >= 0 && dev_fail < i)) {
+                i = dev_fail;
+                const double R = r_obs[i] / r_exp;
+                double mu = R <= params->r_min ? 0.0
+                            : R >= params->r_max
+                                ? 1.0
+                                : 0.5 - 0.5 * std::cos((std::numbers::pi / params->r_max) * (R - params->r_min));
+                msg = "alpha_from_mu: mu = " + std::to_string(mu) + " outside [0, 1]";
+            }
+            throw Failure(AIDW_ERR_RUNTIME, "aidw_predict_all: query " + std::to_string(i) + ": " + msg, i);
+        }
+        weighting_stage(ddx.get(), ddy.get(), ddz.get(), m, dqx.get(), dqy.get(), n,
+                        alpha_q.get(), ext, use_fp64(variant, pinned_order), pred.get(),
+                        alpha_o.get(), fails, nullptr, s);
+        d2h(pred_out, pred.get(), n, s);
+        d2h(alpha_out, alpha_o.get(), n, s);
+        ss.sync();
+    });
+}
+
+int aidw_idw_predict_all(const double* qx, const double* qy, size_t n, const double* dx,
+                         const double* dy, const double* dz, size_t m, double alpha,
+                         int32_t variant, int32_t pinned_order, double* pred_out,
+                         double* alpha_out, aidw_error* err) {
+    return guarded(err, [&] {
+        if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set is empty");
+        if (!dz) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set carries no values");
+        if (!(alpha > 0.0) || !std::isfinite(alpha))
+            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "idw_predict_all: alpha must be positive finite");
+        if (n == 0) return;
+        StreamScope ss;
+        cudaStream_t s = ss.s;
+        FailFlags fails(s);
+        DBuf<double> ddx, ddy, ddz, dqx, dqy, alpha_q(n, s), pred(n, s), alpha_o(n, s);
+        h2d(ddx, dx, m, s);
+        h2d(ddy, dy, m, s);
+        h2d(ddz, dz, m, s);
+        h2d(dqx, qx, n, s);
+        h2d(dqy, qy, n, s);
+        const Extents ext = extents(ddx.get(), ddy.get(), m, dqx.get(), dqy.get(), n, ddz.get(), m, s);
+        LAUNCH(fill_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, alpha_q.get(), n, alpha);
+        weighting_stage(ddx.get(), ddy.get(), ddz.get(), m, dqx.get(), dqy.get(), n,
+                        alpha_q.get(), ext, use_fp64(variant, pinned_order), pred.get(),
+                        alpha_o.get(), fails, nullptr, s);
+        d2h(pred_out, pred.get(), n, s);
+        d2h(alpha_out, alpha_o.get(), n, s);
+        ss.sync();
+    });
+}
+
+int aidw_run_pipeline(const double* dx, const double* dy, const double* dz, size_t m,
+                      const double* qx, const double* qy, size_t n, const aidw_run_config* cfg,
+                      double* pred_out, double* alpha_out, aidw_run_stats* stats,
+                      aidw_error* err) {
+    return guarded(err, [&] {
+        if (!cfg) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "run_pipeline: config missing");
+        const auto t0 = std::chrono::steady_clock::now();
+        StreamScope ss;
+        cudaStream_t s = ss.s;
+        DBuf<double> ddx, ddy, ddz, dqx, dqy, pred(n, s), alpha(n, s);
+        h2d(ddx, dx, m, s);
+        h2d(ddy, dy, m, s);
+        if (dz) h2d(ddz, dz, m, s);
+        h2d(dqx, qx, n, s);
+        h2d(dqy, qy, n, s);
+        ss.sync();
+        const double h2d_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        PipelineIO io{ddx.get(), ddy.get(), dz ? ddz.get() : nullptr, dqx.get(), dqy.get(), m, n,
+                      pred.get(), alpha.get()};
+        pipeline_entry(io, *cfg, stats, s, h2d_ms, t0, pred_out, alpha_out);
+    });
+}
+
+int aidw_run_pipeline_device(const double* d_dx, const double* d_dy, const double* d_dz,
+                             size_t m, const double* d_qx, const double* d_qy, size_t n,
+                             const aidw_run_config* cfg, double* d_pred, double* d_alpha,
+                             aidw_run_stats* stats, void* stream, aidw_error* err) {
+    return guarded(err, [&] {
+        if (!cfg) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "run_pipeline: config missing");
+        const auto t0 = std::chrono::steady_clock::now();
+        StreamScope ss(stream);
+        PipelineIO io{d_dx, d_dy, d_dz, d_qx, d_qy, m, n, d_pred, d_alpha};
+        pipeline_entry(io, *cfg, stats, ss.s, 0.0, t0, nullptr, nullptr);
+    });
+}
+
+int aidw_compute_bbox_device(const double* d_dx, const double* d_dy, size_t m,
+                             const double* d_qx, const double* d_qy, size_t n, double* out,
+                             void* stream, aidw_error* err) {
+    return guarded(err, [&] {
+        if (m == 0 && n == 0)
+            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "compute_bbox: both point sets are empty");
+        StreamScope ss(stream);
+        const Extents e = extents(d_dx, d_dy, m, d_qx, d_qy, n, nullptr, 0, ss.s);
+        out[0] = e.box.min_x;
+        out[1] = e.box.min_y;
+        out[2] = e.box.max_x;
+        out[3] = e.box.max_y;
+    });
+}
+
+}  // extern "C"

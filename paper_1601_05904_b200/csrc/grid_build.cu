@@ -1,0 +1,364 @@
+// grid_build.cu — K1: even-grid construction on sm_100a.
+//
+// Replaces build_index (proj/include/aidw/grid.hpp:176-213): the reference
+// runs a sequential counting sort (locate -> histogram -> prefix -> stable
+// scatter).  Here the same CSR arrays come from
+//   1. cell_ids_kernel  : FP64 locate_cell per point (exact reference
+//                         rounding), key = row-major cell id, value = index,
+//                         per-cell histogram with global atomics;
+//   2. exclusive_scan   : cell_start = exclusive prefix of the histogram;
+//   3. radix_sort_pairs : stable LSD radix sort (8-bit digits, warp-level
+//                         __match_any ranking) of (cell id, index) -> ids
+//                         grouped by cell, ascending index within a cell;
+//   4. gather_kernel    : cell-sorted copies of x / y.
+// All arrays are bit-identical to the reference's (tests/test_gpu_parity.py).
+// Compiled with -fmad=false: every FP64 expression keeps the reference's
+// two-rounding form.
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace aidwb {
+
+namespace {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 8;  // per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;  // 2048 keys
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kThreads * kScanItems;  // 2048 values
+
+__global__ void cell_ids_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                size_t m, GridGeom g, uint32_t* __restrict__ keys,
+                                uint32_t* __restrict__ vals, uint32_t* __restrict__ counts,
+                                long long* __restrict__ fail) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    int col, row;
+    uint32_t cell = 0;
+    if (locate_cell_dev(x[i], y[i], g, col, row)) {
+        cell = static_cast<uint32_t>(row) * static_cast<uint32_t>(g.n_col) +
+               static_cast<uint32_t>(col);
+        if (counts) atomicAdd(&counts[cell], 1u);
+    } else {
+        atomicMin(fail, static_cast<long long>(i));
+    }
+    keys[i] = cell;
+    vals[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void gather_kernel(const uint32_t* __restrict__ order, const double* __restrict__ x,
+                              const double* __restrict__ y, size_t m,
+                              uint32_t* __restrict__ ids, double* __restrict__ sx,
+                              double* __restrict__ sy) {
+    const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    const uint32_t id = order[s];
+    ids[s] = id;
+    sx[s] = x[id];
+    sy[s] = y[id];
+}
+
+// ---------------------------------------------------------------- scan
+__device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Block-local exclusive scan of a 2048-value tile; tile totals -> sums.
+__global__ void scan_tiles_kernel(const uint32_t* in, uint32_t* out, size_t n,
+                                  uint32_t* __restrict__ sums) {
+    __shared__ uint32_t warp_total[kThreads / 32];
+    const size_t base = static_cast<size_t>(blockIdx.x) * kScanTile +
+                        static_cast<size_t>(threadIdx.x) * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t run = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const size_t idx = base + j;
+        v[j] = idx < n ? in[idx] : 0u;
+        run += v[j];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t incl = warp_inclusive_scan(run);
+    if (lane == 31) warp_total[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t t = lane < kThreads / 32 ? warp_total[lane] : 0u;
+        t = warp_inclusive_scan(t);
+        if (lane < kThreads / 32) warp_total[lane] = t;
+    }
+    __syncthreads();
+    uint32_t prefix = incl - run + (warp > 0 ? warp_total[warp - 1] : 0u);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const size_t idx = base + j;
+        if (idx < n) out[idx] = prefix;
+        prefix += v[j];
+    }
+    if (threadIdx.x == kThreads - 1 && sums) sums[blockIdx.x] = prefix;
+}
+
+__global__ void add_tile_offsets_kernel(uint32_t* out, size_t n,
+                                        const uint32_t* __restrict__ offsets) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] += offsets[i / kScanTile];
+}
+
+// ---------------------------------------------------------------- radix sort
+// Per tile: histogram of the digit -> hist[digit * tiles + tile].
+__global__ void radix_upsweep_kernel(const uint32_t* __restrict__ keys, size_t n, int shift,
+                                     uint32_t* __restrict__ hist, unsigned tiles) {
+    __shared__ uint32_t h[kRadix];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const size_t base = static_cast<size_t>(blockIdx.x) * kSortTile;
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const size_t idx = base + static_cast<size_t>(j) * kSortThreads + threadIdx.x;
+        if (idx < n) atomicAdd(&h[(keys[idx] >> shift) & (kRadix - 1)], 1u);
+    }
+    __syncthreads();
+    hist[static_cast<size_t>(threadIdx.x) * tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter: warp w owns keys [tile + w*256, +256), taken 32 at a time
+// in index order; a key's rank = (same digit in earlier warps) + (same digit
+// in earlier rounds of this warp) + (same digit in lower lanes this round).
+__global__ void radix_scatter_kernel(const uint32_t* __restrict__ keys_in,
+                                     const uint32_t* __restrict__ vals_in,
+                                     uint32_t* __restrict__ keys_out,
+                                     uint32_t* __restrict__ vals_out, size_t n, int shift,
+                                     const uint32_t* __restrict__ offsets, unsigned tiles) {
+    __shared__ uint32_t cnt[kSortWarps][kRadix];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) cnt[w][threadIdx.x] = 0;
+    __syncthreads();
+
+    const size_t base = static_cast<size_t>(blockIdx.x) * kSortTile +
+                        static_cast<size_t>(warp) * (32 * kSortItems);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t k[kSortItems], v[kSortItems], rank[kSortItems];
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const size_t idx = base + static_cast<size_t>(r) * 32 + lane;
+        const bool valid = idx < n;
+        k[r] = valid ? keys_in[idx] : 0u;
+        v[r] = valid ? vals_in[idx] : 0u;
+        const uint32_t d = valid ? ((k[r] >> shift) & (kRadix - 1)) : kRadix;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        const uint32_t before = valid ? cnt[warp][d] : 0u;
+        rank[r] = before + __popc(peers & lt_mask);
+        __syncwarp();
+        if (valid && (__ffs(peers) - 1) == lane) cnt[warp][d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) {
+            const uint32_t c = cnt[w][threadIdx.x];
+            cnt[w][threadIdx.x] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const size_t idx = base + static_cast<size_t>(r) * 32 + lane;
+        if (idx < n) {
+            const uint32_t d = (k[r] >> shift) & (kRadix - 1);
+            const size_t pos = static_cast<size_t>(offsets[static_cast<size_t>(d) * tiles + blockIdx.x]) +
+                               cnt[warp][d] + rank[r];
+            keys_out[pos] = k[r];
+            vals_out[pos] = v[r];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- min / max
+__device__ __forceinline__ unsigned long long order_key(double d) {
+    const unsigned long long u = as_u64(d);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+// keys[0..2] = min x, y, z ; keys[3..5] = max x, y, z (order-preserving u64
+// encoding; NaNs are skipped like std::min/max in compute_bbox).
+__global__ void minmax_kernel(const double* __restrict__ ax, const double* __restrict__ ay,
+                              size_t na, const double* __restrict__ bx,
+                              const double* __restrict__ by, size_t nb,
+                              const double* __restrict__ z, size_t nz,
+                              unsigned long long* __restrict__ keys) {
+    unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0ull, 0ull, 0ull};
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t start = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t total = na + nb;
+    for (size_t i = start; i < total; i += stride) {
+        const double x = i < na ? ax[i] : bx[i - na];
+        const double y = i < na ? ay[i] : by[i - na];
+        if (x == x) {
+            const unsigned long long kx = order_key(x);
+            lo[0] = kx < lo[0] ? kx : lo[0];
+            hi[0] = kx > hi[0] ? kx : hi[0];
+        }
+        if (y == y) {
+            const unsigned long long ky = order_key(y);
+            lo[1] = ky < lo[1] ? ky : lo[1];
+            hi[1] = ky > hi[1] ? ky : hi[1];
+        }
+    }
+    for (size_t i = start; i < nz; i += stride) {
+        const double v = z[i];
+        if (v == v) {
+            const unsigned long long kz = order_key(v);
+            lo[2] = kz < lo[2] ? kz : lo[2];
+            hi[2] = kz > hi[2] ? kz : hi[2];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        lo[q] = warp_min_u64(lo[q]);
+        hi[q] = warp_max_u64(hi[q]);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            atomicMin(&keys[q], lo[q]);
+            atomicMax(&keys[3 + q], hi[q]);
+        }
+    }
+}
+
+__global__ void decode_minmax_kernel(const unsigned long long* __restrict__ keys,
+                                     double* __restrict__ out6) {
+    // out6 = {min_x, min_y, max_x, max_y, min_z, max_z}
+    const int map[6] = {0, 1, 3, 4, 2, 5};
+    const int t = threadIdx.x;
+    if (t < 6) {
+        const unsigned long long k = keys[map[t]];
+        const unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+        out6[t] = __longlong_as_double(static_cast<long long>(u));
+    }
+}
+
+int bits_for(uint64_t max_key) {
+    int b = 0;
+    while (b < 32 && (max_key >> b) != 0) ++b;
+    return b;
+}
+
+}  // namespace
+
+void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, size_t n, cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned tiles = ceil_div(n, kScanTile);
+    if (tiles == 1) {
+        LAUNCH(scan_tiles_kernel, 1, kThreads, 0, s, d_in, d_out, n, nullptr);
+        return;
+    }
+    DBuf<uint32_t> sums(tiles, s);
+    LAUNCH(scan_tiles_kernel, tiles, kThreads, 0, s, d_in, d_out, n, sums.get());
+    exclusive_scan_u32(sums.get(), sums.get(), tiles, s);
+    LAUNCH(add_tile_offsets_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_out, n, sums.get());
+}
+
+void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaStream_t s) {
+    if (n <= 1 || bits <= 0) return;
+    const int passes = (bits + kRadixBits - 1) / kRadixBits;
+    const unsigned tiles = ceil_div(n, kSortTile);
+    DBuf<uint32_t> k2(n, s), v2(n, s), hist(static_cast<size_t>(kRadix) * tiles, s);
+    uint32_t *ki = keys, *vi = vals, *ko = k2.get(), *vo = v2.get();
+    for (int p = 0; p < passes; ++p) {
+        const int shift = p * kRadixBits;
+        LAUNCH(radix_upsweep_kernel, tiles, kSortThreads, 0, s, ki, n, shift, hist.get(), tiles);
+        exclusive_scan_u32(hist.get(), hist.get(), static_cast<size_t>(kRadix) * tiles, s);
+        LAUNCH(radix_scatter_kernel, tiles, kSortThreads, 0, s, ki, vi, ko, vo, n, shift,
+               hist.get(), tiles);
+        std::swap(ki, ko);
+        std::swap(vi, vo);
+    }
+    if (ki != keys) {
+        CK(cudaMemcpyAsync(keys, ki, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(vals, vi, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+void build_grid_device(const double* d_x, const double* d_y, size_t m,
+                       const aidw_grid_config& cfg, DeviceGrid& out, long long* d_fail,
+                       cudaStream_t s) {
+    const GridGeom g = make_geom(cfg);
+    const size_t cells = static_cast<size_t>(cfg.n_col) * static_cast<size_t>(cfg.n_row);
+    out.cfg = cfg;
+    out.m = m;
+    out.cells = cells;
+    out.cell_start.alloc(cells + 1, s);
+    out.sorted_ids.alloc(m, s);
+    out.sorted_x.alloc(m, s);
+    out.sorted_y.alloc(m, s);
+    DBuf<uint32_t> keys(m, s), vals(m, s);
+    CK(cudaMemsetAsync(out.cell_start.get(), 0, (cells + 1) * sizeof(uint32_t), s));
+    LAUNCH(cell_ids_kernel, ceil_div(m, kThreads), kThreads, 0, s, d_x, d_y, m, g, keys.get(),
+           vals.get(), out.cell_start.get(), d_fail);
+    exclusive_scan_u32(out.cell_start.get(), out.cell_start.get(), cells + 1, s);
+    radix_sort_pairs(keys.get(), vals.get(), m, bits_for(cells - 1), s);
+    LAUNCH(gather_kernel, ceil_div(m, kThreads), kThreads, 0, s, vals.get(), d_x, d_y, m,
+           out.sorted_ids.get(), out.sorted_x.get(), out.sorted_y.get());
+}
+
+void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, const GridGeom& g,
+                          DBuf<uint32_t>& perm, DBuf<uint32_t>& cells, long long* d_fail,
+                          cudaStream_t s) {
+    perm.alloc(n, s);
+    cells.alloc(n, s);
+    if (n == 0) return;
+    LAUNCH(cell_ids_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_qx, d_qy, n, g,
+           cells.get(), perm.get(), static_cast<uint32_t*>(nullptr), d_fail);
+    const size_t total = static_cast<size_t>(g.n_col) * static_cast<size_t>(g.n_row);
+    radix_sort_pairs(cells.get(), perm.get(), n, bits_for(total - 1), s);
+}
+
+void bbox_reduce_device(const double* d_ax, const double* d_ay, size_t na, const double* d_bx,
+                        const double* d_by, size_t nb, const double* d_z, size_t nz,
+                        double* d_out6, cudaStream_t s) {
+    DBuf<unsigned long long> keys(6, s);
+    CK(cudaMemsetAsync(keys.get(), 0xFF, 3 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(keys.get() + 3, 0, 3 * sizeof(unsigned long long), s));
+    const size_t total = na + nb > nz ? na + nb : nz;
+    unsigned blocks = ceil_div(total ? total : 1, kThreads * 8);
+    if (blocks > 148u * 8u) blocks = 148u * 8u;
+    LAUNCH(minmax_kernel, blocks, kThreads, 0, s, d_ax, d_ay, na, d_bx, d_by, nb, d_z, nz,
+           keys.get());
+    LAUNCH(decode_minmax_kernel, 1, 32, 0, s, keys.get(), d_out6);
+}
+
+}  // namespace aidwb

@@ -1,0 +1,392 @@
+// weight.cu — K4: the O(m·n) inverse-distance weighting on sm_100a (FP32).
+//
+// Replaces the weighting loops of aidw_predict_all / idw_predict_all
+// (proj/include/aidw/interpolate.hpp:252-381, :426-489).  Design:
+//
+//  * Data records live in HBM as {x_hi, y_hi, x_lo, y_lo} float4 + z float,
+//    coordinates normalised to the unit box in FP64 first and split into an
+//    FP32 hi/lo pair, so dx = (x_hi - q_hi) + (x_lo - q_lo) keeps ~48 bits
+//    without any FP64 op or F2F conversion per pair.  Padded to 256-point
+//    tiles with records at 1e30 (weight exactly 0).
+//  * Each CTA (256 threads, QT queries per thread in registers) streams the
+//    tiles of one data chunk through a NSTAGE-deep shared-memory ring filled
+//    by the bulk-copy engine (cp.async.bulk + mbarrier complete_tx; SASS
+//    UBLKCP), one elected thread producing, all warps consuming broadcast
+//    LDS.128 reads.
+//  * Ratio scaling: w' = (d2 / d2_min)^(-alpha/2) <= 1, evaluated as
+//    ex2(c * lg2(d2) + b) with c = -alpha/2, b = -c * lg2(d2_min) — two MUFU
+//    ops (MUFU.LG2, MUFU.EX2) + 9 FP32 ops per pair.  Queries with
+//    alpha == 4 exactly (98 % of uniform-data queries, the reference's
+//    half-integer recipe, interpolate.hpp:174-209) use w' = rcp((d2*s)^2),
+//    one MUFU.  Queries are partitioned so warps are class-uniform; the
+//    formula is chosen per query, never per warp, so results do not depend
+//    on the partition (or on the GPU count).
+//  * Per-tile FP32 sums are folded into FP64 accumulators; data chunks
+//    (S = f(m) only) give enough CTAs at small n and are summed in chunk
+//    order by the settle kernel, deterministically (no atomics).
+//  * settle: snap -> z[first index within snap distance]; analytic overflow
+//    test in log space reproduces the FP64 reference's non-finite sums ->
+//    nearest value (lowest index on ties); clamp to the value hull.
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+#include "weight.cuh"
+
+namespace aidwb {
+
+namespace {
+
+constexpr int kQT = 4;          // queries per thread
+constexpr int kK4Threads = 256;
+constexpr int kStages = 4;
+constexpr int kMaxChunks = 16;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ float mufu_lg2(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float mufu_ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float mufu_rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// ------------------------------------------------------------ record prep
+__device__ __forceinline__ void split_hilo(double v, float& hi, float& lo) {
+    hi = __double2float_rn(v);
+    lo = __double2float_rn(v - static_cast<double>(hi));
+}
+
+__global__ void prep_data_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                 const double* __restrict__ z, size_t m, size_t mp, double ox,
+                                 double oy, double inv_scale, double zmul,
+                                 float4* __restrict__ xy, float* __restrict__ zz) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= mp) return;
+    if (i < m) {
+        float xh, xl, yh, yl;
+        split_hilo((x[i] - ox) * inv_scale, xh, xl);
+        split_hilo((y[i] - oy) * inv_scale, yh, yl);
+        xy[i] = make_float4(xh, yh, xl, yl);
+        zz[i] = __double2float_rn(z[i] * zmul);
+    } else {
+        xy[i] = make_float4(1.0e30f, 1.0e30f, 0.0f, 0.0f);
+        zz[i] = 0.0f;
+    }
+}
+
+std::atomic<bool> g_alpha4_recipe{true};
+
+// class A: the exact alpha == 4 recipe (or snapped: result replaced anyway)
+__global__ void class_flags_kernel(const double* __restrict__ alpha_s,
+                                   const uint32_t* __restrict__ snap_s, size_t n, int recipe,
+                                   uint32_t* __restrict__ flag) {
+    const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    flag[p] = ((recipe && alpha_s[p] == 4.0) || snap_s[p] != kNoId) ? 1u : 0u;
+}
+
+// Stable partition (class A first) fused with the per-query record build.
+__global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
+                                     const uint32_t* __restrict__ flag,
+                                     const uint32_t* __restrict__ scan_a,
+                                     uint32_t* __restrict__ order, float4* __restrict__ qhl,
+                                     float4* __restrict__ qpar,
+                                     unsigned long long* __restrict__ alpha4) {
+    const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= q.n) return;
+    const size_t num_a = static_cast<size_t>(scan_a[q.n - 1]) + flag[q.n - 1];
+    const bool is_a = flag[p] != 0;
+    const size_t i = is_a ? scan_a[p] : num_a + (p - scan_a[p]);
+    order[i] = static_cast<uint32_t>(p);
+    const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
+    float xh, xl, yh, yl;
+    split_hilo((q.qx[qi] - f.ox) * f.inv_scale, xh, xl);
+    split_hilo((q.qy[qi] - f.oy) * f.inv_scale, yh, yl);
+    qhl[i] = make_float4(xh, yh, xl, yl);
+    const double alpha = q.alpha_s[p];
+    const double d2n = q.d2min_s[p] * f.inv_scale * f.inv_scale;
+    const double c = -0.5 * alpha;
+    const float b = __double2float_rn(-c * log2(d2n));
+    const float s = __double2float_rn(1.0 / d2n);
+    qpar[i] = make_float4(__double2float_rn(c), b, s, is_a ? 1.0f : 0.0f);
+    if (alpha == 4.0 && alpha4) atomicAdd(alpha4, 1ull);
+}
+
+// ------------------------------------------------------------ K4
+struct K4Args {
+    const float4* xy;
+    const float* z;
+    size_t tiles, tiles_per_chunk;
+    unsigned chunks;
+    const float4* qhl;
+    const float4* qpar;
+    size_t n;
+    double2* part;  // n * chunks
+};
+
+template <int MODE>  // 0: all recipe, 1: all general, 2: per-query select
+__device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
+                                        const float* __restrict__ tz, const float (&qxh)[kQT],
+                                        const float (&qyh)[kQT], const float (&qxl)[kQT],
+                                        const float (&qyl)[kQT], const float (&qc)[kQT],
+                                        const float (&qb)[kQT], const float (&qs)[kQT],
+                                        const bool (&qa)[kQT], float (&sw)[kQT],
+                                        float (&swz)[kQT]) {
+#pragma unroll 4
+    for (int j = 0; j < kWeightTile; ++j) {
+        const float4 p = txy[j];
+        const float zz = tz[j];
+#pragma unroll
+        for (int q = 0; q < kQT; ++q) {
+            const float dx = (p.x - qxh[q]) + (p.z - qxl[q]);
+            const float dy = (p.y - qyh[q]) + (p.w - qyl[q]);
+            const float d2 = fmaf(dx, dx, dy * dy);
+            float w;
+            if (MODE == 0) {
+                const float t = d2 * qs[q];
+                w = mufu_rcp(t * t);
+            } else if (MODE == 1) {
+                w = mufu_ex2(fmaf(qc[q], mufu_lg2(d2), qb[q]));
+            } else {
+                const float t = d2 * qs[q];
+                w = qa[q] ? mufu_rcp(t * t) : mufu_ex2(fmaf(qc[q], mufu_lg2(d2), qb[q]));
+            }
+            sw[q] += w;
+            swz[q] = fmaf(w, zz, swz[q]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float4* sxy = reinterpret_cast<float4*>(smem);
+    float* sz = reinterpret_cast<float*>(sxy + kStages * kWeightTile);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sz + kStages * kWeightTile);
+
+    const unsigned chunk = blockIdx.y;
+    const size_t t0 = static_cast<size_t>(chunk) * a.tiles_per_chunk;
+    const size_t t1 = t0 + a.tiles_per_chunk < a.tiles ? t0 + a.tiles_per_chunk : a.tiles;
+    const size_t ntl = t1 > t0 ? t1 - t0 : 0;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t wbase = static_cast<size_t>(blockIdx.x) * (kK4Threads * kQT) +
+                         static_cast<size_t>(warp) * (32 * kQT);
+    float qxh[kQT], qyh[kQT], qxl[kQT], qyl[kQT], qc[kQT], qb[kQT], qs[kQT];
+    bool qa[kQT];
+    bool any_a = false, any_g = false;
+#pragma unroll
+    for (int q = 0; q < kQT; ++q) {
+        const size_t p = wbase + static_cast<size_t>(q) * 32 + lane;
+        float4 h = make_float4(0.f, 0.f, 0.f, 0.f), r = make_float4(-1.f, 0.f, 1.f, 1.f);
+        if (p < a.n) {
+            h = a.qhl[p];
+            r = a.qpar[p];
+            qa[q] = r.w != 0.0f;
+            any_a |= qa[q];
+            any_g |= !qa[q];
+        } else {
+            qa[q] = true;
+        }
+        qxh[q] = h.x;
+        qyh[q] = h.y;
+        qxl[q] = h.z;
+        qyl[q] = h.w;
+        qc[q] = r.x;
+        qb[q] = r.y;
+        qs[q] = r.z;
+    }
+    any_a = __any_sync(0xFFFFFFFFu, any_a);
+    any_g = __any_sync(0xFFFFFFFFu, any_g);
+    const int mode = any_g ? (any_a ? 2 : 1) : 0;
+
+    double SW[kQT], SWZ[kQT];
+#pragma unroll
+    for (int q = 0; q < kQT; ++q) SW[q] = SWZ[q] = 0.0;
+
+    constexpr uint32_t kXYBytes = kWeightTile * sizeof(float4);
+    constexpr uint32_t kZBytes = kWeightTile * sizeof(float);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (size_t s = 0; s < ntl && s < static_cast<size_t>(kStages); ++s) {
+            mbar_expect_tx(&bar[s], kXYBytes + kZBytes);
+            bulk_load(sxy + s * kWeightTile, a.xy + (t0 + s) * kWeightTile, kXYBytes, &bar[s]);
+            bulk_load(sz + s * kWeightTile, a.z + (t0 + s) * kWeightTile, kZBytes, &bar[s]);
+        }
+    }
+    for (size_t it = 0; it < ntl; ++it) {
+        const int st = static_cast<int>(it % kStages);
+        mbar_wait(&bar[st], static_cast<uint32_t>((it / kStages) & 1));
+        const float4* txy = sxy + st * kWeightTile;
+        const float* tz = sz + st * kWeightTile;
+        float sw[kQT], swz[kQT];
+#pragma unroll
+        for (int q = 0; q < kQT; ++q) sw[q] = swz[q] = 0.0f;
+        if (mode == 0) {
+            k4_tile<0>(txy, tz, qxh, qyh, qxl, qyl, qc, qb, qs, qa, sw, swz);
+        } else if (mode == 1) {
+            k4_tile<1>(txy, tz, qxh, qyh, qxl, qyl, qc, qb, qs, qa, sw, swz);
+        } else {
+            k4_tile<2>(txy, tz, qxh, qyh, qxl, qyl, qc, qb, qs, qa, sw, swz);
+        }
+#pragma unroll
+        for (int q = 0; q < kQT; ++q) {
+            SW[q] += static_cast<double>(sw[q]);
+            SWZ[q] += static_cast<double>(swz[q]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && it + kStages < ntl) {
+            fence_proxy_async();
+            const size_t tile = t0 + it + kStages;
+            mbar_expect_tx(&bar[st], kXYBytes + kZBytes);
+            bulk_load(sxy + st * kWeightTile, a.xy + tile * kWeightTile, kXYBytes, &bar[st]);
+            bulk_load(sz + st * kWeightTile, a.z + tile * kWeightTile, kZBytes, &bar[st]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kQT; ++q) {
+        const size_t p = wbase + static_cast<size_t>(q) * 32 + lane;
+        if (p < a.n) a.part[p * a.chunks + chunk] = make_double2(SW[q], SWZ[q]);
+    }
+}
+
+// ------------------------------------------------------------ settle
+__global__ void settle_kernel(const WeightQueries q, WeightFrame f, const WeightData d,
+                              const uint32_t* __restrict__ order,
+                              const double2* __restrict__ part, unsigned chunks,
+                              double* __restrict__ pred, double* __restrict__ alpha_out) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= q.n) return;
+    const uint32_t p = order[i];
+    const uint32_t qi = q.perm ? q.perm[p] : p;
+    const double alpha = q.alpha_s[p];
+    double out;
+    const uint32_t snap = q.snap_s[p];
+    if (snap != kNoId) {
+        out = d.z[snap];
+    } else {
+        double sw = 0.0, swz = 0.0;
+        for (unsigned c = 0; c < chunks; ++c) {
+            const double2 v = part[static_cast<size_t>(i) * chunks + c];
+            sw += v.x;
+            swz += v.y;
+        }
+        // log2 of the reference's (unscaled, FP64) weight sums:
+        //   w_max = d2_min^(-alpha/2), sum_w = w_max * sw, sum_wz = w_max * swz / 2^zshift
+        const double e = -0.5 * alpha * log2(q.d2min_s[p]);
+        bool fallback = !(sw > 0.0) || !isfinite(sw) || !isfinite(swz) || !(e < 1024.0) ||
+                        !(e + log2(sw) < 1024.0) || e < -1075.0;
+        if (!fallback && swz != 0.0 && !(e + log2(fabs(swz)) - f.zshift < 1024.0)) fallback = true;
+        if (fallback) {
+            out = d.z[q.nn_s[p]];
+        } else {
+            double v = ldexp(swz / sw, -f.zshift);
+            out = v < f.zlo ? f.zlo : (v > f.zhi ? f.zhi : v);
+        }
+    }
+    pred[qi] = out;
+    if (alpha_out) alpha_out[qi] = alpha;
+}
+
+}  // namespace
+
+void set_alpha4_recipe(bool enabled) { g_alpha4_recipe.store(enabled); }
+
+WeightSplit weight_split(size_t m) {
+    WeightSplit w;
+    w.tiles = (m + kWeightTile - 1) / kWeightTile;
+    if (w.tiles == 0) w.tiles = 1;
+    size_t chunks = w.tiles < static_cast<size_t>(kMaxChunks) ? w.tiles : kMaxChunks;
+    w.tiles_per_chunk = (w.tiles + chunks - 1) / chunks;
+    w.chunks = static_cast<unsigned>((w.tiles + w.tiles_per_chunk - 1) / w.tiles_per_chunk);
+    return w;
+}
+
+void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFrame& f,
+                    double* d_pred, double* d_alpha, WeightTimes* times, cudaStream_t s) {
+    if (q.n == 0) return;
+    const WeightSplit sp = weight_split(d.m);
+    const size_t mp = sp.tiles * kWeightTile;
+    DBuf<float4> xy(mp, s);
+    DBuf<float> zz(mp, s);
+    LAUNCH(prep_data_kernel, ceil_div(mp, kThreads), kThreads, 0, s, d.x, d.y, d.z, d.m, mp,
+           f.ox, f.oy, f.inv_scale, std::ldexp(1.0, f.zshift), xy.get(), zz.get());
+
+    DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), order(q.n, s);
+    DBuf<float4> qhl(q.n, s), qpar(q.n, s);
+    LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q.alpha_s, q.snap_s, q.n,
+           g_alpha4_recipe.load() ? 1 : 0, flag.get());
+    exclusive_scan_u32(flag.get(), scan_a.get(), q.n, s);
+    LAUNCH(query_records_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, flag.get(),
+           scan_a.get(), order.get(), qhl.get(), qpar.get(),
+           times ? times->d_alpha4 : nullptr);
+
+    DBuf<double2> part(q.n * sp.chunks, s);
+    K4Args ka{xy.get(), zz.get(), sp.tiles, sp.tiles_per_chunk, sp.chunks, qhl.get(), qpar.get(),
+              q.n, part.get()};
+    const size_t smem = kStages * kWeightTile * (sizeof(float4) + sizeof(float)) +
+                        kStages * sizeof(uint64_t);
+    CK(cudaFuncSetAttribute(weight_fp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    dim3 grid(ceil_div(q.n, kK4Threads * kQT), sp.chunks);
+    if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+    LAUNCH(weight_fp32_kernel, grid, kK4Threads, smem, s, ka);
+    if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
+    LAUNCH(settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order.get(),
+           part.get(), sp.chunks, d_pred, d_alpha);
+}
+
+}  // namespace aidwb

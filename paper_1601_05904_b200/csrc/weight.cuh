@@ -1,0 +1,72 @@
+// weight.cuh — the weighting stage (K4) interface.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace aidwb {
+
+// Normalisation frame of the FP32 path: X = (x - ox) * inv_scale maps the
+// bbox into [0, 1]; z' = z * 2^zshift keeps |z'| <= 1 (exact scaling).
+struct WeightFrame {
+    double ox = 0.0, oy = 0.0, inv_scale = 1.0;
+    int zshift = 0;
+    double zlo = 0.0, zhi = 0.0;  // value hull (interpolate.hpp:73-80)
+    double snap_sq = 0.0;         // interpolate.hpp:86-89 (FP64 path)
+};
+
+// Per-query inputs of the weighting stage, in visiting order `pos`
+// (perm[pos] = query index; perm == nullptr means identity).
+struct WeightQueries {
+    const double* qx = nullptr;  // query index order
+    const double* qy = nullptr;
+    size_t n = 0;
+    const uint32_t* perm = nullptr;
+    const double* alpha_s = nullptr;   // by pos
+    const double* d2min_s = nullptr;   // by pos (FP32 path)
+    const uint32_t* nn_s = nullptr;    // by pos (FP32 path)
+    const uint32_t* snap_s = nullptr;  // by pos (FP32 path)
+};
+
+struct WeightData {
+    const double* x = nullptr;  // index order
+    const double* y = nullptr;
+    const double* z = nullptr;
+    size_t m = 0;
+};
+
+// Optional instrumentation: events recorded around the K4 launch(es) and a
+// device counter of recipe-path queries; the caller resolves them after its
+// final synchronisation (no mid-pipeline host sync).
+struct WeightTimes {
+    cudaEvent_t k4_begin = nullptr, k4_end = nullptr;
+    unsigned long long* d_alpha4 = nullptr;
+};
+
+// FP32 MUFU path (Variant::blocked default).  Writes pred/alpha by query
+// index.  When `times` is non-null the K4 launches are bracketed by events.
+void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFrame& f,
+                    double* d_pred, double* d_alpha, WeightTimes* times, cudaStream_t s);
+
+// FP64 path (Variant::naive, pinned_order, AIDW_WEIGHT_FP64): index-order
+// accumulation with 1 / pow(sqrt(d2), alpha), reference snap / fallback.
+void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFrame& f,
+                    double* d_pred, double* d_alpha, WeightTimes* times, cudaStream_t s);
+
+// Chunking of the data set for the FP32 kernel; depends on m only, so the
+// per-query summation order is independent of n and of the GPU count.
+struct WeightSplit {
+    size_t tiles = 0;            // padded m / kWeightTile
+    unsigned chunks = 1;         // S
+    size_t tiles_per_chunk = 0;
+};
+WeightSplit weight_split(size_t m);
+constexpr int kWeightTile = 256;
+
+// Global switch of the alpha == 4 one-MUFU recipe (aidw_set_alpha4_recipe).
+void set_alpha4_recipe(bool enabled);
+
+}  // namespace aidwb
