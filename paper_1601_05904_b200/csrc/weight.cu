@@ -174,35 +174,99 @@ struct K4Args {
     double2* part;  // n * chunks
 };
 
-template <int MODE>  // 0: all recipe, 1: all general, 2: per-query select
+// ---- packed f32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2): two queries per
+// 64-bit register pair; each lane rounds exactly like the scalar op, so a
+// query's result does not depend on which lane / pair it occupies.
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+constexpr int kPairs = kQT / 2;
+
+// Per-thread query state: kQT queries as kPairs f32x2 pairs.
+struct QState {
+    f2 xh[kPairs], yh[kPairs], xl[kPairs], yl[kPairs];
+    f2 c[kPairs], b[kPairs], s[kPairs];
+    bool a[kQT];  // recipe class, per query
+};
+
+// One 256-point tile against the thread's kQT queries.  Per data point and
+// query pair: 3 FADD2 (dx), 3 FADD2 (dy), FMUL2 + FFMA2 (d2), then
+//   MODE 0 (alpha == 4 recipe): FMUL2 (d2 s), FMUL2 (^2), 2 x MUFU.RCP
+//   MODE 1 (general):           2 x MUFU.LG2, FFMA2 (c lg + b), 2 x MUFU.EX2
+//   MODE 2 (mixed warp):        per query, scalar, same roundings
+// and FADD2 (sum w) + FFMA2 (sum w z).
+template <int MODE>
 __device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
-                                        const float* __restrict__ tz, const float (&qxh)[kQT],
-                                        const float (&qyh)[kQT], const float (&qxl)[kQT],
-                                        const float (&qyl)[kQT], const float (&qc)[kQT],
-                                        const float (&qb)[kQT], const float (&qs)[kQT],
-                                        const bool (&qa)[kQT], float (&sw)[kQT],
-                                        float (&swz)[kQT]) {
-#pragma unroll 4
+                                        const float* __restrict__ tz, const QState& q,
+                                        f2 (&sw)[kPairs], f2 (&swz)[kPairs]) {
+#pragma unroll 2
     for (int j = 0; j < kWeightTile; ++j) {
         const float4 p = txy[j];
         const float zz = tz[j];
+        const f2 px = pk2(p.x, p.x), py = pk2(p.y, p.y), pxl = pk2(p.z, p.z),
+                 pyl = pk2(p.w, p.w), pz = pk2(zz, zz);
 #pragma unroll
-        for (int q = 0; q < kQT; ++q) {
-            const float dx = (p.x - qxh[q]) + (p.z - qxl[q]);
-            const float dy = (p.y - qyh[q]) + (p.w - qyl[q]);
-            const float d2 = fmaf(dx, dx, dy * dy);
-            float w;
+        for (int r = 0; r < kPairs; ++r) {
+            const f2 dx = add2(sub2(px, q.xh[r]), sub2(pxl, q.xl[r]));
+            const f2 dy = add2(sub2(py, q.yh[r]), sub2(pyl, q.yl[r]));
+            const f2 d2 = fma2(dx, dx, mul2(dy, dy));
+            f2 w;
             if (MODE == 0) {
-                const float t = d2 * qs[q];
-                w = mufu_rcp(t * t);
+                const f2 t = mul2(d2, q.s[r]);
+                float lo, hi;
+                up2(mul2(t, t), lo, hi);
+                w = pk2(mufu_rcp(lo), mufu_rcp(hi));
             } else if (MODE == 1) {
-                w = mufu_ex2(fmaf(qc[q], mufu_lg2(d2), qb[q]));
+                float lo, hi;
+                up2(d2, lo, hi);
+                up2(fma2(q.c[r], pk2(mufu_lg2(lo), mufu_lg2(hi)), q.b[r]), lo, hi);
+                w = pk2(mufu_ex2(lo), mufu_ex2(hi));
             } else {
-                const float t = d2 * qs[q];
-                w = qa[q] ? mufu_rcp(t * t) : mufu_ex2(fmaf(qc[q], mufu_lg2(d2), qb[q]));
+                float d[2], cc[2], bb[2], ss[2], ww[2];
+                up2(d2, d[0], d[1]);
+                up2(q.c[r], cc[0], cc[1]);
+                up2(q.b[r], bb[0], bb[1]);
+                up2(q.s[r], ss[0], ss[1]);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (q.a[2 * r + h]) {
+                        const float t = d[h] * ss[h];
+                        ww[h] = mufu_rcp(t * t);
+                    } else {
+                        ww[h] = mufu_ex2(fmaf(cc[h], mufu_lg2(d[h]), bb[h]));
+                    }
+                }
+                w = pk2(ww[0], ww[1]);
             }
-            sw[q] += w;
-            swz[q] = fmaf(w, zz, swz[q]);
+            sw[r] = add2(sw[r], w);
+            swz[r] = fma2(w, pz, swz[r]);
         }
     }
 }
@@ -221,29 +285,36 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t wbase = static_cast<size_t>(blockIdx.x) * (kK4Threads * kQT) +
                          static_cast<size_t>(warp) * (32 * kQT);
-    float qxh[kQT], qyh[kQT], qxl[kQT], qyl[kQT], qc[kQT], qb[kQT], qs[kQT];
-    bool qa[kQT];
+    QState q;
     bool any_a = false, any_g = false;
+    {
+        float4 h[kQT], r[kQT];
 #pragma unroll
-    for (int q = 0; q < kQT; ++q) {
-        const size_t p = wbase + static_cast<size_t>(q) * 32 + lane;
-        float4 h = make_float4(0.f, 0.f, 0.f, 0.f), r = make_float4(-1.f, 0.f, 1.f, 1.f);
-        if (p < a.n) {
-            h = a.qhl[p];
-            r = a.qpar[p];
-            qa[q] = r.w != 0.0f;
-            any_a |= qa[q];
-            any_g |= !qa[q];
-        } else {
-            qa[q] = true;
+        for (int i = 0; i < kQT; ++i) {
+            const size_t p = wbase + static_cast<size_t>(i) * 32 + lane;
+            h[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            r[i] = make_float4(-1.f, 0.f, 1.f, 1.f);
+            if (p < a.n) {
+                h[i] = a.qhl[p];
+                r[i] = a.qpar[p];
+                q.a[i] = r[i].w != 0.0f;
+                any_a |= q.a[i];
+                any_g |= !q.a[i];
+            } else {
+                q.a[i] = true;
+            }
         }
-        qxh[q] = h.x;
-        qyh[q] = h.y;
-        qxl[q] = h.z;
-        qyl[q] = h.w;
-        qc[q] = r.x;
-        qb[q] = r.y;
-        qs[q] = r.z;
+#pragma unroll
+        for (int k = 0; k < kPairs; ++k) {
+            const int i0 = 2 * k, i1 = 2 * k + 1;
+            q.xh[k] = pk2(h[i0].x, h[i1].x);
+            q.yh[k] = pk2(h[i0].y, h[i1].y);
+            q.xl[k] = pk2(h[i0].z, h[i1].z);
+            q.yl[k] = pk2(h[i0].w, h[i1].w);
+            q.c[k] = pk2(r[i0].x, r[i1].x);
+            q.b[k] = pk2(r[i0].y, r[i1].y);
+            q.s[k] = pk2(r[i0].z, r[i1].z);
+        }
     }
     any_a = __any_sync(0xFFFFFFFFu, any_a);
     any_g = __any_sync(0xFFFFFFFFu, any_g);
@@ -251,7 +322,7 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
 
     double SW[kQT], SWZ[kQT];
 #pragma unroll
-    for (int q = 0; q < kQT; ++q) SW[q] = SWZ[q] = 0.0;
+    for (int i = 0; i < kQT; ++i) SW[i] = SWZ[i] = 0.0;
 
     constexpr uint32_t kXYBytes = kWeightTile * sizeof(float4);
     constexpr uint32_t kZBytes = kWeightTile * sizeof(float);
@@ -272,20 +343,25 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
         mbar_wait(&bar[st], static_cast<uint32_t>((it / kStages) & 1));
         const float4* txy = sxy + st * kWeightTile;
         const float* tz = sz + st * kWeightTile;
-        float sw[kQT], swz[kQT];
+        f2 sw[kPairs], swz[kPairs];
 #pragma unroll
-        for (int q = 0; q < kQT; ++q) sw[q] = swz[q] = 0.0f;
+        for (int k = 0; k < kPairs; ++k) sw[k] = swz[k] = 0ull;
         if (mode == 0) {
-            k4_tile<0>(txy, tz, qxh, qyh, qxl, qyl, qc, qb, qs, qa, sw, swz);
+            k4_tile<0>(txy, tz, q, sw, swz);
         } else if (mode == 1) {
-            k4_tile<1>(txy, tz, qxh, qyh, qxl, qyl, qc, qb, qs, qa, sw, swz);
+            k4_tile<1>(txy, tz, q, sw, swz);
         } else {
-            k4_tile<2>(txy, tz, qxh, qyh, qxl, qyl, qc, qb, qs, qa, sw, swz);
+            k4_tile<2>(txy, tz, q, sw, swz);
         }
 #pragma unroll
-        for (int q = 0; q < kQT; ++q) {
-            SW[q] += static_cast<double>(sw[q]);
-            SWZ[q] += static_cast<double>(swz[q]);
+        for (int k = 0; k < kPairs; ++k) {
+            float lo, hi;
+            up2(sw[k], lo, hi);
+            SW[2 * k] += static_cast<double>(lo);
+            SW[2 * k + 1] += static_cast<double>(hi);
+            up2(swz[k], lo, hi);
+            SWZ[2 * k] += static_cast<double>(lo);
+            SWZ[2 * k + 1] += static_cast<double>(hi);
         }
         __syncthreads();
         if (threadIdx.x == 0 && it + kStages < ntl) {
@@ -297,9 +373,9 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
         }
     }
 #pragma unroll
-    for (int q = 0; q < kQT; ++q) {
-        const size_t p = wbase + static_cast<size_t>(q) * 32 + lane;
-        if (p < a.n) a.part[p * a.chunks + chunk] = make_double2(SW[q], SWZ[q]);
+    for (int i = 0; i < kQT; ++i) {
+        const size_t p = wbase + static_cast<size_t>(i) * 32 + lane;
+        if (p < a.n) a.part[p * a.chunks + chunk] = make_double2(SW[i], SWZ[i]);
     }
 }
 
