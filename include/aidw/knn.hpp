@@ -20,6 +20,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "aidw/executor.hpp"
@@ -214,13 +215,29 @@ inline std::vector<KnnResult> knn_stage(const PointSet& queries, const GridIndex
                        grid ? AIDW_ENGINE_GRID : AIDW_ENGINE_BRUTE, d2.data(), nullptr, avg.data(),
                        &k_eff, &exhausted, &err),
         err);
+    // Materialise n heap vectors (the API's KnnResult shape).  This is host
+    // allocation work, spread over the hardware threads (glibc arenas scale).
     std::vector<KnnResult> out(n);
     const auto ke = static_cast<std::size_t>(std::max(k_eff, 0));
-    for (std::size_t i = 0; i < n; ++i) {
-        out[i].distances_sq.assign(d2.begin() + static_cast<std::ptrdiff_t>(i * ke),
-                                   d2.begin() + static_cast<std::ptrdiff_t>((i + 1) * ke));
-        out[i].average_distance = avg[i];
-        out[i].exhausted = exhausted != 0;
+    auto fill = [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            out[i].distances_sq.assign(d2.begin() + static_cast<std::ptrdiff_t>(i * ke),
+                                       d2.begin() + static_cast<std::ptrdiff_t>((i + 1) * ke));
+            out[i].average_distance = avg[i];
+            out[i].exhausted = exhausted != 0;
+        }
+    };
+    const std::size_t threads =
+        std::min<std::size_t>(static_cast<std::size_t>(resolve_workers(0)), n / 8192 + 1);
+    if (threads <= 1) {
+        fill(0, n);
+    } else {
+        std::vector<std::thread> pool;
+        const std::size_t step = (n + threads - 1) / threads;
+        for (std::size_t t = 0; t < threads; ++t) {
+            pool.emplace_back(fill, std::min(n, t * step), std::min(n, (t + 1) * step));
+        }
+        for (auto& th : pool) th.join();
     }
     return out;
 }

@@ -143,6 +143,17 @@ int current_device() {
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t thr = std::numeric_limits<uint64_t>::max();
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            // Reserve a working set once (freed memory stays in the pool), so
+            // later calls never pay pool growth inside a timed stage.
+            size_t free_b = 0, total_b = 0;
+            if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+                const size_t want = std::min<size_t>(free_b / 8, size_t(8) << 30);
+                void* p = nullptr;
+                if (want && cudaMallocAsync(&p, want, 0) == cudaSuccess) {
+                    cudaFreeAsync(p, 0);
+                    cudaStreamSynchronize(0);
+                }
+            }
         }
     });
     return dev;
@@ -298,26 +309,30 @@ __global__ void fill_f64_kernel(double* __restrict__ dst, size_t n, double v) {
     if (i < n) dst[i] = v;
 }
 
-bool use_fp64(int32_t variant, int32_t pinned) {
-    return variant == AIDW_VARIANT_NAIVE || pinned != 0 ||
-           g_precision.load(std::memory_order_relaxed) == AIDW_PRECISION_FP64;
+// Which weighting kernel a (variant, pinned_order) call runs.
+enum class WeightMode { fp32, fp64_blocked, fp64_naive };
+WeightMode weight_mode(int32_t variant, int32_t pinned) {
+    if (variant == AIDW_VARIANT_NAIVE || pinned != 0) return WeightMode::fp64_naive;
+    return g_precision.load(std::memory_order_relaxed) == AIDW_PRECISION_FP64
+               ? WeightMode::fp64_blocked
+               : WeightMode::fp32;
 }
 
 // Weighting stage over device-resident inputs given alpha by query index.
 // d_alpha_q: alpha per query (input order).
 void weighting_stage(const double* d_dx, const double* d_dy, const double* d_dz, size_t m,
                      const double* d_qx, const double* d_qy, size_t n, const double* d_alpha_q,
-                     const Extents& ext, bool fp64, double* d_pred, double* d_alpha_out,
+                     const Extents& ext, WeightMode mode, double* d_pred, double* d_alpha_out,
                      FailFlags& fails, WeightTimes* wt, cudaStream_t s) {
     const WeightFrame frame = make_frame(ext.box, ext.zlo, ext.zhi);
     WeightData wd{d_dx, d_dy, d_dz, m};
-    if (fp64) {
+    if (mode != WeightMode::fp32) {
         WeightQueries q;
         q.qx = d_qx;
         q.qy = d_qy;
         q.n = n;
         q.alpha_s = d_alpha_q;
-        weighting_fp64(q, wd, frame, d_pred, d_alpha_out, wt, s);
+        weighting_fp64(q, wd, frame, mode == WeightMode::fp64_blocked, d_pred, d_alpha_out, wt, s);
         return;
     }
     NearestInfo nb;
@@ -388,7 +403,7 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     CK(cudaMemsetAsync(a4buf.get(), 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(candbuf.get(), 0, sizeof(unsigned long long), s));
     d_a4 = a4buf.get();
-    const bool fp64 = use_fp64(cfg.variant, 0);
+    const WeightMode wmode = weight_mode(cfg.variant, 0);
     WeightTimes wt;
     wt.k4_begin = k4b = ev.make();
     wt.k4_end = k4e = ev.make();
@@ -414,7 +429,7 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
         CK(cudaEventRecord(e_knn1, s));
         DBuf<double> alpha_q(n, s);
         if (n) LAUNCH(fill_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, alpha_q.get(), n, cfg.alpha);
-        weighting_stage(io.dx, io.dy, io.dz, m, io.qx, io.qy, n, alpha_q.get(), ext, fp64,
+        weighting_stage(io.dx, io.dy, io.dz, m, io.qx, io.qy, n, alpha_q.get(), ext, wmode,
                         io.pred, io.alpha, fails, &wt, s);
         CK(cudaEventRecord(e_interp1, s));
         fails.fetch(s);
@@ -502,8 +517,8 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     q.d2min_s = d2min_s.get();
     q.nn_s = nn_s.get();
     q.snap_s = snap_s.get();
-    if (fp64)
-        weighting_fp64(q, wd, frame, io.pred, io.alpha, &wt, s);
+    if (wmode != WeightMode::fp32)
+        weighting_fp64(q, wd, frame, wmode == WeightMode::fp64_blocked, io.pred, io.alpha, &wt, s);
     else
         weighting_fp32(q, wd, frame, io.pred, io.alpha, &wt, s);
     CK(cudaEventRecord(e_interp1, s));
@@ -775,7 +790,7 @@ int aidw_aidw_predict_all(const double* qx, const double* qy, size_t n, const do
             throw Failure(AIDW_ERR_RUNTIME, "aidw_predict_all: query " + std::to_string(i) + ": " + msg, i);
         }
         weighting_stage(ddx.get(), ddy.get(), ddz.get(), m, dqx.get(), dqy.get(), n,
-                        alpha_q.get(), ext, use_fp64(variant, pinned_order), pred.get(),
+                        alpha_q.get(), ext, weight_mode(variant, pinned_order), pred.get(),
                         alpha_o.get(), fails, nullptr, s);
         d2h(pred_out, pred.get(), n, s);
         d2h(alpha_out, alpha_o.get(), n, s);
@@ -805,7 +820,7 @@ int aidw_idw_predict_all(const double* qx, const double* qy, size_t n, const dou
         const Extents ext = extents(ddx.get(), ddy.get(), m, dqx.get(), dqy.get(), n, ddz.get(), m, s);
         LAUNCH(fill_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, alpha_q.get(), n, alpha);
         weighting_stage(ddx.get(), ddy.get(), ddz.get(), m, dqx.get(), dqy.get(), n,
-                        alpha_q.get(), ext, use_fp64(variant, pinned_order), pred.get(),
+                        alpha_q.get(), ext, weight_mode(variant, pinned_order), pred.get(),
                         alpha_o.get(), fails, nullptr, s);
         d2h(pred_out, pred.get(), n, s);
         d2h(alpha_out, alpha_o.get(), n, s);

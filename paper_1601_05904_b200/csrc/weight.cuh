@@ -53,8 +53,11 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
 
 // FP64 path (Variant::naive, pinned_order, AIDW_WEIGHT_FP64): index-order
 // accumulation with 1 / pow(sqrt(d2), alpha), reference snap / fallback.
+// `blocked` selects the reference's blocked-variant arithmetic (recipe /
+// exp-log, chunked sums) instead of the naive pow form.
 void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFrame& f,
-                    double* d_pred, double* d_alpha, WeightTimes* times, cudaStream_t s);
+                    bool blocked, double* d_pred, double* d_alpha, WeightTimes* times,
+                    cudaStream_t s);
 
 // Chunking of the data set for the FP32 kernel; depends on m only, so the
 // per-query summation order is independent of n and of the GPU count.
