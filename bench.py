@@ -126,8 +126,9 @@ def make_inputs(A, cfg, world, rank):
     else:
         data = A.generate_random_points(m, UNIT, 42)
         allq = A.generate_random_queries(n * world, UNIT, 43)
-    sl = slice(rank * n, (rank + 1) * n)
-    return data, A.PointSet(allq.xs[sl].copy(), allq.ys[sl].copy())
+    from paper_1601_05904_b200.shard import shard_range
+    lo, hi = shard_range(n * world, world, rank)
+    return data, A.PointSet(allq.xs[lo:hi].copy(), allq.ys[lo:hi].copy())
 
 
 def reference_cpu(cfg, data, queries, target_s=8.0, workers=0):
@@ -240,10 +241,11 @@ def main():
     data, queries = make_inputs(A, cfg, world, rank)
     m, n = data.count(), queries.count()
 
+    from paper_1601_05904_b200 import shard
+
     # data: rank 0's copy replicated over NVLink (NCCL broadcast)
     d_data = torch.from_numpy(np.stack([data.xs, data.ys, data.zs])).to(dev)
-    if world > 1:
-        dist.broadcast(d_data, src=0)
+    shard.replicate(d_data, dist if world > 1 else None)
     d_q = torch.from_numpy(np.stack([queries.xs, queries.ys])).to(dev)
     d_pred = torch.empty(n, dtype=torch.float64, device=dev)
     d_alpha = torch.empty(n, dtype=torch.float64, device=dev)
@@ -253,12 +255,8 @@ def main():
     qx, qy = d_q[0].data_ptr(), d_q[1].data_ptr()
 
     # global bbox(data ∪ all queries): per-rank device reduce + all-reduce
-    bb = A.compute_bbox_device(dx, dy, m, qx, qy, n, sp)
-    if world > 1:
-        t = torch.tensor([bb[0], bb[1], -bb[2], -bb[3]], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        v = t.tolist()
-        bb = np.array([v[0], v[1], -v[2], -v[3]])
+    bb = shard.global_bbox(A.compute_bbox_device(dx, dy, m, qx, qy, n, sp),
+                           dist if world > 1 else None, device=dev)
     rc = A.RunConfig(params=A.AidwParams(k=cfg["k"]), bbox=tuple(float(v) for v in bb))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
