@@ -32,6 +32,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 
 #include "common.cuh"
@@ -41,7 +42,6 @@ namespace aidwb {
 
 namespace {
 
-constexpr int kQT = 4;          // queries per thread
 constexpr int kK4Threads = 256;
 constexpr int kStages = 4;
 constexpr int kMaxChunks = 16;
@@ -140,7 +140,7 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
                                      const uint32_t* __restrict__ flag,
                                      const uint32_t* __restrict__ scan_a,
                                      uint32_t* __restrict__ order, float4* __restrict__ qhl,
-                                     float4* __restrict__ qpar,
+                                     float4* __restrict__ qpar, double* __restrict__ lshift,
                                      unsigned long long* __restrict__ alpha4) {
     const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p >= q.n) return;
@@ -155,10 +155,19 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
     qhl[i] = make_float4(xh, yh, xl, yl);
     const double alpha = q.alpha_s[p];
     const double d2n = q.d2min_s[p] * f.inv_scale * f.inv_scale;
-    const double c = -0.5 * alpha;
-    const float b = __double2float_rn(-c * log2(d2n));
-    const float s = __double2float_rn(1.0 / d2n);
-    qpar[i] = make_float4(__double2float_rn(c), b, s, is_a ? 1.0f : 0.0f);
+    const float c = __double2float_rn(-0.5 * alpha);
+    // general path: w' = ex2(c lg2(d2) + b) with b = -c lg2(d2min) so w' <= 1
+    const float b = __double2float_rn(-static_cast<double>(c) * log2(d2n));
+    // recipe path: w' = rcp((d2 s)^2).  s = 1 (no multiply needed, exact)
+    // whenever d2 >= d2min >= 1e-15 keeps d2^2 and 1/d2^2 inside FP32;
+    // otherwise s = 1/d2min.  Snapped queries: result replaced, s = 1.
+    const bool snapped = q.snap_s[p] != kNoId;
+    const float s = (snapped || d2n >= 1.0e-15) ? 1.0f : __double2float_rn(1.0 / d2n);
+    qpar[i] = make_float4(c, b, s, is_a ? 1.0f : 0.0f);
+    // log2(true weight) = log2(kernel weight) + shift (settle's overflow test)
+    const double l2inv = log2(f.inv_scale);
+    lshift[i] = is_a ? 2.0 * log2(static_cast<double>(s)) + 4.0 * l2inv
+                     : -static_cast<double>(b) - 2.0 * static_cast<double>(c) * l2inv;
     if (alpha == 4.0 && alpha4) atomicAdd(alpha4, 1ull);
 }
 
@@ -207,25 +216,27 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
     return r;
 }
 
-constexpr int kPairs = kQT / 2;
-
-// Per-thread query state: kQT queries as kPairs f32x2 pairs.
+// Per-thread query state: QT queries as QT/2 f32x2 pairs.
+template <int QT>
 struct QState {
+    static constexpr int kPairs = QT / 2;
     f2 xh[kPairs], yh[kPairs], xl[kPairs], yl[kPairs];
     f2 c[kPairs], b[kPairs], s[kPairs];
-    bool a[kQT];  // recipe class, per query
+    bool a[QT];  // recipe class, per query
 };
 
 // One 256-point tile against the thread's kQT queries.  Per data point and
 // query pair: 3 FADD2 (dx), 3 FADD2 (dy), FMUL2 + FFMA2 (d2), then
-//   MODE 0 (alpha == 4 recipe): FMUL2 (d2 s), FMUL2 (^2), 2 x MUFU.RCP
+//   MODE 3 (alpha == 4 recipe, s == 1): FMUL2 (d2^2), 2 x MUFU.RCP
+//   MODE 0 (alpha == 4 recipe, scaled): FMUL2 (d2 s), FMUL2 (^2), 2 x MUFU.RCP
 //   MODE 1 (general):           2 x MUFU.LG2, FFMA2 (c lg + b), 2 x MUFU.EX2
 //   MODE 2 (mixed warp):        per query, scalar, same roundings
 // and FADD2 (sum w) + FFMA2 (sum w z).
-template <int MODE>
+template <int MODE, int QT>
 __device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
-                                        const float* __restrict__ tz, const QState& q,
-                                        f2 (&sw)[kPairs], f2 (&swz)[kPairs]) {
+                                        const float* __restrict__ tz, const QState<QT>& q,
+                                        f2 (&sw)[QT / 2], f2 (&swz)[QT / 2]) {
+    constexpr int kPairs = QT / 2;
 #pragma unroll 2
     for (int j = 0; j < kWeightTile; ++j) {
         const float4 p = txy[j];
@@ -238,7 +249,11 @@ __device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
             const f2 dy = add2(sub2(py, q.yh[r]), sub2(pyl, q.yl[r]));
             const f2 d2 = fma2(dx, dx, mul2(dy, dy));
             f2 w;
-            if (MODE == 0) {
+            if (MODE == 3) {  // recipe, s == 1 for every query of the warp
+                float lo, hi;
+                up2(mul2(d2, d2), lo, hi);
+                w = pk2(mufu_rcp(lo), mufu_rcp(hi));
+            } else if (MODE == 0) {
                 const f2 t = mul2(d2, q.s[r]);
                 float lo, hi;
                 up2(mul2(t, t), lo, hi);
@@ -271,7 +286,9 @@ __device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
     }
 }
 
-__global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
+template <int kQT, int kMinBlocks>
+__global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4Args a) {
+    constexpr int kPairs = kQT / 2;
     extern __shared__ __align__(128) unsigned char smem[];
     float4* sxy = reinterpret_cast<float4*>(smem);
     float* sz = reinterpret_cast<float*>(sxy + kStages * kWeightTile);
@@ -285,8 +302,8 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t wbase = static_cast<size_t>(blockIdx.x) * (kK4Threads * kQT) +
                          static_cast<size_t>(warp) * (32 * kQT);
-    QState q;
-    bool any_a = false, any_g = false;
+    QState<kQT> q;
+    bool any_a = false, any_g = false, any_scaled = false;
     {
         float4 h[kQT], r[kQT];
 #pragma unroll
@@ -300,6 +317,7 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
                 q.a[i] = r[i].w != 0.0f;
                 any_a |= q.a[i];
                 any_g |= !q.a[i];
+                any_scaled |= r[i].z != 1.0f;
             } else {
                 q.a[i] = true;
             }
@@ -318,7 +336,11 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
     }
     any_a = __any_sync(0xFFFFFFFFu, any_a);
     any_g = __any_sync(0xFFFFFFFFu, any_g);
-    const int mode = any_g ? (any_a ? 2 : 1) : 0;
+    any_scaled = __any_sync(0xFFFFFFFFu, any_scaled);
+    // warp-uniform formula group; per query the arithmetic is identical in
+    // every mode (s == 1 makes d2 * s == d2 exactly), so grouping never
+    // changes a result
+    const int mode = any_g ? (any_a ? 2 : 1) : (any_scaled ? 0 : 3);
 
     double SW[kQT], SWZ[kQT];
 #pragma unroll
@@ -346,12 +368,14 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
         f2 sw[kPairs], swz[kPairs];
 #pragma unroll
         for (int k = 0; k < kPairs; ++k) sw[k] = swz[k] = 0ull;
-        if (mode == 0) {
-            k4_tile<0>(txy, tz, q, sw, swz);
+        if (mode == 3) {
+            k4_tile<3, kQT>(txy, tz, q, sw, swz);
+        } else if (mode == 0) {
+            k4_tile<0, kQT>(txy, tz, q, sw, swz);
         } else if (mode == 1) {
-            k4_tile<1>(txy, tz, q, sw, swz);
+            k4_tile<1, kQT>(txy, tz, q, sw, swz);
         } else {
-            k4_tile<2>(txy, tz, q, sw, swz);
+            k4_tile<2, kQT>(txy, tz, q, sw, swz);
         }
 #pragma unroll
         for (int k = 0; k < kPairs; ++k) {
@@ -382,7 +406,8 @@ __global__ void __launch_bounds__(kK4Threads, 2) weight_fp32_kernel(K4Args a) {
 // ------------------------------------------------------------ settle
 __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const WeightData d,
                               const uint32_t* __restrict__ order,
-                              const double2* __restrict__ part, unsigned chunks,
+                              const double2* __restrict__ part,
+                              const double* __restrict__ lshift, unsigned chunks,
                               double* __restrict__ pred, double* __restrict__ alpha_out) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= q.n) return;
@@ -400,12 +425,14 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
             sw += v.x;
             swz += v.y;
         }
-        // log2 of the reference's (unscaled, FP64) weight sums:
-        //   w_max = d2_min^(-alpha/2), sum_w = w_max * sw, sum_wz = w_max * swz / 2^zshift
+        // The FP64 reference overflows / underflows where the true (unscaled)
+        // weights do (interpolate.hpp:109-118): its largest weight is
+        // 2^e, e = -alpha/2 log2 d2_min; its sums are 2^lshift * (sw, swz / 2^zshift).
         const double e = -0.5 * alpha * log2(q.d2min_s[p]);
+        const double sh = lshift[i];
         bool fallback = !(sw > 0.0) || !isfinite(sw) || !isfinite(swz) || !(e < 1024.0) ||
-                        !(e + log2(sw) < 1024.0) || e < -1075.0;
-        if (!fallback && swz != 0.0 && !(e + log2(fabs(swz)) - f.zshift < 1024.0)) fallback = true;
+                        !(sh + log2(sw) < 1024.0) || e < -1075.0;
+        if (!fallback && swz != 0.0 && !(sh + log2(fabs(swz)) - f.zshift < 1024.0)) fallback = true;
         if (fallback) {
             out = d.z[q.nn_s[p]];
         } else {
@@ -443,11 +470,12 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
 
     DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), order(q.n, s);
     DBuf<float4> qhl(q.n, s), qpar(q.n, s);
+    DBuf<double> lshift(q.n, s);
     LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q.alpha_s, q.snap_s, q.n,
            g_alpha4_recipe.load() ? 1 : 0, flag.get());
     exclusive_scan_u32(flag.get(), scan_a.get(), q.n, s);
     LAUNCH(query_records_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, flag.get(),
-           scan_a.get(), order.get(), qhl.get(), qpar.get(),
+           scan_a.get(), order.get(), qhl.get(), qpar.get(), lshift.get(),
            times ? times->d_alpha4 : nullptr);
 
     DBuf<double2> part(q.n * sp.chunks, s);
@@ -455,14 +483,33 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
               q.n, part.get()};
     const size_t smem = kStages * kWeightTile * (sizeof(float4) + sizeof(float)) +
                         kStages * sizeof(uint64_t);
-    CK(cudaFuncSetAttribute(weight_fp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    dim3 grid(ceil_div(q.n, kK4Threads * kQT), sp.chunks);
-    if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
-    LAUNCH(weight_fp32_kernel, grid, kK4Threads, smem, s, ka);
+    // K4 variant: queries per thread x min resident CTAs (AIDW_K4_VARIANT for
+    // tuning; default 4x2).  Per-query arithmetic is identical in all.
+    static const int variant = [] {
+        const char* v = std::getenv("AIDW_K4_VARIANT");
+        return v ? std::atoi(v) : 0;
+    }();
+    auto launch = [&](auto kernel, int qt) {
+        CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        dim3 grid(ceil_div(q.n, static_cast<size_t>(kK4Threads) * qt), sp.chunks);
+        if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+        LAUNCH(kernel, grid, kK4Threads, smem, s, ka);
+    };
+    switch (variant) {
+        case 1: launch(weight_fp32_kernel<8, 1>, 8); break;
+        case 2: launch(weight_fp32_kernel<4, 3>, 4); break;
+        case 3: launch(weight_fp32_kernel<2, 3>, 2); break;
+        case 4: launch(weight_fp32_kernel<8, 2>, 8); break;
+        case 5: launch(weight_fp32_kernel<4, 4>, 4); break;
+        case 6: launch(weight_fp32_kernel<2, 4>, 2); break;
+        case 7: launch(weight_fp32_kernel<6, 2>, 6); break;
+        case 8: launch(weight_fp32_kernel<4, 2>, 4); break;
+        default: launch(weight_fp32_kernel<4, 3>, 4); break;
+    }
     if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
     LAUNCH(settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order.get(),
-           part.get(), sp.chunks, d_pred, d_alpha);
+           part.get(), lshift.get(), sp.chunks, d_pred, d_alpha);
 }
 
 }  // namespace aidwb
