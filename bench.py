@@ -295,10 +295,12 @@ def main():
     peak_gpairs = sms * 8 * f_mhz * 1e6 / 1e9  # 2 MUFU / pair, 16 MUFU / clk / SM
     achieved = pairs / (k4_ms / 1e3) / 1e9
     knn_ms = statistics.median(s["knn_kernel_ms"] for s in stats)
-    cand = stats[-1]["knn_candidates"]
-    knn_bytes = n * (16 + 8 + 8 + 4 + 4) + 16 * cand  # query in, candidates, alpha/d2min/nn/snap out
+    cand = stats[-1]["knn_candidates"]  # points K2 actually scanned (after cell pruning)
+    ref_cand = stats[-1]["knn_ref_candidates"]  # points the reference scans (final-level blocks)
+    # SURVEY §8d algorithmic bytes: 16 B query + 16 B per reference candidate + outputs
+    knn_bytes = n * (16 + 8 + 8 + 4 + 4) + 16 * ref_cand
     build_ms = statistics.median(s["build_ms"] for s in stats)
-    build_bytes = 64 * m + 8 * (cfg["m"] // 16 + 1)
+    build_bytes = 64 * m + 8 * (m // 4 + 1)  # factor-4 grid: ~m/4 cells (SURVEY §8 grid table)
     a4 = stats[-1]["alpha4_queries"]
 
     # general-alpha path forced (every query on exp2/log2), reported separately
@@ -362,7 +364,7 @@ def main():
                 "knn_hbm": {"bytes": knn_bytes, "achieved_gbs": knn_bytes / (knn_ms / 1e3) / 1e9,
                             "peak_gbs": pk["hbm_gbs"],
                             "frac": knn_bytes / (knn_ms / 1e3) / 1e9 / pk["hbm_gbs"],
-                            "candidates": cand},
+                            "candidates_reference": ref_cand, "candidates_scanned": cand},
                 "build_hbm": {"bytes": build_bytes,
                               "achieved_gbs": build_bytes / (build_ms / 1e3) / 1e9,
                               "frac": build_bytes / (build_ms / 1e3) / 1e9 / pk["hbm_gbs"]},

@@ -107,6 +107,7 @@ typedef struct {
     int32_t worker_count;
     int64_t pairs;           /* m * n weighting pairs evaluated        */
     int64_t knn_candidates;  /* candidates scanned by K2 (sum over queries) */
+    int64_t knn_ref_candidates; /* candidates the reference scans: final-level blocks */
     int64_t alpha4_queries;  /* queries on the exact alpha = 4 recipe  */
     int64_t kernel_launches; /* kernels launched by this call          */
 } aidw_run_stats;

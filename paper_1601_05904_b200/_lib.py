@@ -54,7 +54,8 @@ class RunStats(C.Structure):
                 ("total_ms", C.c_double), ("weight_kernel_ms", C.c_double),
                 ("knn_kernel_ms", C.c_double), ("h2d_ms", C.c_double), ("d2h_ms", C.c_double),
                 ("k_effective", C.c_int32), ("worker_count", C.c_int32), ("pairs", C.c_int64),
-                ("knn_candidates", C.c_int64), ("alpha4_queries", C.c_int64),
+                ("knn_candidates", C.c_int64), ("knn_ref_candidates", C.c_int64),
+                ("alpha4_queries", C.c_int64),
                 ("kernel_launches", C.c_int64)]
 
     def as_dict(self):

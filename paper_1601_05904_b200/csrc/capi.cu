@@ -291,8 +291,7 @@ void nearest_search(const double* d_dx, const double* d_dy, size_t m, const doub
     a.g = geom;
     a.cell_start = g.cell_start.get();
     a.sorted_ids = g.sorted_ids.get();
-    a.sorted_x = g.sorted_x.get();
-    a.sorted_y = g.sorted_y.get();
+    a.sorted_xy = g.sorted_xy.get();
     a.perm = out.perm.get();
     a.qcell = qcell.get();
     run_knn_grid(a, s);
@@ -399,9 +398,9 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     if (!io.dz) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set carries no values");
     FailFlags fails(s);
     a4buf.alloc(1, s);
-    candbuf.alloc(1, s);
+    candbuf.alloc(2, s);
     CK(cudaMemsetAsync(a4buf.get(), 0, sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(candbuf.get(), 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(candbuf.get(), 0, 2 * sizeof(unsigned long long), s));
     d_a4 = a4buf.get();
     const WeightMode wmode = weight_mode(cfg.variant, 0);
     WeightTimes wt;
@@ -453,6 +452,7 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     a.k = k;
     a.k_eff = k;
     a.candidates = candbuf.get();
+    a.ref_candidates = candbuf.get() + 1;
     const double area = params.area > 0.0 ? params.area : ext.box.area();
     const double r_exp_arg = static_cast<double>(m) / area;
     if (!(area > 0.0) || !std::isfinite(area))
@@ -487,8 +487,7 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
         a.g = geom;
         a.cell_start = g.cell_start.get();
         a.sorted_ids = g.sorted_ids.get();
-        a.sorted_x = g.sorted_x.get();
-        a.sorted_y = g.sorted_y.get();
+        a.sorted_xy = g.sorted_xy.get();
         a.perm = perm.get();
         a.qcell = qcell.get();
         CK(cudaEventRecord(knnb, s));
@@ -574,8 +573,10 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
         if (a4buf.get()) CK(cudaMemcpy(&h, a4buf.get(), sizeof h, cudaMemcpyDeviceToHost));
         st->alpha4_queries = static_cast<int64_t>(h);
         h = 0;
-        if (candbuf.get()) CK(cudaMemcpy(&h, candbuf.get(), sizeof h, cudaMemcpyDeviceToHost));
-        st->knn_candidates = static_cast<int64_t>(h);
+        unsigned long long hc[2] = {0, 0};
+        if (candbuf.get()) CK(cudaMemcpy(hc, candbuf.get(), sizeof hc, cudaMemcpyDeviceToHost));
+        st->knn_candidates = static_cast<int64_t>(hc[0]);
+        st->knn_ref_candidates = static_cast<int64_t>(hc[1]);
         st->kernel_launches = g_launches.load() - launches0;
         st->total_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -630,7 +631,7 @@ int aidw_build_index(const double* xs, const double* ys, size_t m, const aidw_gr
         h2d(dx, xs, m, s);
         h2d(dy, ys, m, s);
         DeviceGrid g;
-        build_grid_device(dx.get(), dy.get(), m, *cfg, g, fails.slot(kFailData), s);
+        build_grid_device(dx.get(), dy.get(), m, *cfg, g, fails.slot(kFailData), s, true);
         fails.fetch(s);
         if (fails.h[kFailData] != LLONG_MAX) {
             const long long i = fails.h[kFailData];
@@ -688,6 +689,7 @@ int aidw_knn_stage(const double* qx, const double* qy, size_t n, const aidw_grid
         a.id_out = idx_out ? ids.get() : nullptr;
         a.avg_out = avg.get();
         DBuf<double> ddx, ddy, sx, sy;
+        DBuf<double2> sxy;
         DBuf<uint32_t> cs, sid, perm, qcell;
         if (grid) {
             const size_t cells = static_cast<size_t>(cfg->n_col) * static_cast<size_t>(cfg->n_row);
@@ -706,8 +708,9 @@ int aidw_knn_stage(const double* qx, const double* qy, size_t n, const aidw_grid
             a.g = geom;
             a.cell_start = cs.get();
             a.sorted_ids = sid.get();
-            a.sorted_x = sx.get();
-            a.sorted_y = sy.get();
+            sxy.alloc(m, s);
+            interleave_xy(sx.get(), sy.get(), m, sxy.get(), s);
+            a.sorted_xy = sxy.get();
             a.perm = perm.get();
             a.qcell = qcell.get();
             run_knn_grid(a, s);

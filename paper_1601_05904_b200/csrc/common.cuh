@@ -135,14 +135,18 @@ struct DeviceGrid {
     size_t m = 0, cells = 0;
     DBuf<uint32_t> cell_start;  // cells + 1
     DBuf<uint32_t> sorted_ids;  // m
-    DBuf<double> sorted_x, sorted_y;
+    DBuf<double> sorted_x, sorted_y;  // API outputs (only when requested)
+    DBuf<double2> sorted_xy;          // interleaved copy the kNN kernel reads
 };
 
 // Builds the CSR grid from device x/y (m points).  Out-of-region points
 // set *d_fail (atomicMin of the point index); the caller checks it.
 void build_grid_device(const double* d_x, const double* d_y, size_t m,
                        const aidw_grid_config& cfg, DeviceGrid& out, long long* d_fail,
-                       cudaStream_t s);
+                       cudaStream_t s, bool split_coords = false);
+
+// xy[i] = {x[i], y[i]}
+void interleave_xy(const double* d_x, const double* d_y, size_t n, double2* d_xy, cudaStream_t s);
 
 // Sort n query points by cell: returns the permutation (sorted position ->
 // query index) and the sorted cell ids; failures -> *d_fail.

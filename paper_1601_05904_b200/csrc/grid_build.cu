@@ -55,14 +55,24 @@ __global__ void cell_ids_kernel(const double* __restrict__ x, const double* __re
 
 __global__ void gather_kernel(const uint32_t* __restrict__ order, const double* __restrict__ x,
                               const double* __restrict__ y, size_t m,
-                              uint32_t* __restrict__ ids, double* __restrict__ sx,
-                              double* __restrict__ sy) {
+                              uint32_t* __restrict__ ids, double2* __restrict__ sxy,
+                              double* __restrict__ sx, double* __restrict__ sy) {
     const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= m) return;
     const uint32_t id = order[s];
+    const double px = x[id], py = y[id];
     ids[s] = id;
-    sx[s] = x[id];
-    sy[s] = y[id];
+    sxy[s] = make_double2(px, py);
+    if (sx) {
+        sx[s] = px;
+        sy[s] = py;
+    }
+}
+
+__global__ void interleave_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                  size_t n, double2* __restrict__ xy) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) xy[i] = make_double2(x[i], y[i]);
 }
 
 // ---------------------------------------------------------------- scan
@@ -313,9 +323,14 @@ void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaSt
     }
 }
 
+void interleave_xy(const double* d_x, const double* d_y, size_t n, double2* d_xy,
+                   cudaStream_t s) {
+    if (n) LAUNCH(interleave_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_x, d_y, n, d_xy);
+}
+
 void build_grid_device(const double* d_x, const double* d_y, size_t m,
                        const aidw_grid_config& cfg, DeviceGrid& out, long long* d_fail,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool split_coords) {
     const GridGeom g = make_geom(cfg);
     const size_t cells = static_cast<size_t>(cfg.n_col) * static_cast<size_t>(cfg.n_row);
     out.cfg = cfg;
@@ -323,8 +338,11 @@ void build_grid_device(const double* d_x, const double* d_y, size_t m,
     out.cells = cells;
     out.cell_start.alloc(cells + 1, s);
     out.sorted_ids.alloc(m, s);
-    out.sorted_x.alloc(m, s);
-    out.sorted_y.alloc(m, s);
+    out.sorted_xy.alloc(m, s);
+    if (split_coords) {
+        out.sorted_x.alloc(m, s);
+        out.sorted_y.alloc(m, s);
+    }
     DBuf<uint32_t> keys(m, s), vals(m, s);
     CK(cudaMemsetAsync(out.cell_start.get(), 0, (cells + 1) * sizeof(uint32_t), s));
     LAUNCH(cell_ids_kernel, ceil_div(m, kThreads), kThreads, 0, s, d_x, d_y, m, g, keys.get(),
@@ -332,7 +350,7 @@ void build_grid_device(const double* d_x, const double* d_y, size_t m,
     exclusive_scan_u32(out.cell_start.get(), out.cell_start.get(), cells + 1, s);
     radix_sort_pairs(keys.get(), vals.get(), m, bits_for(cells - 1), s);
     LAUNCH(gather_kernel, ceil_div(m, kThreads), kThreads, 0, s, vals.get(), d_x, d_y, m,
-           out.sorted_ids.get(), out.sorted_x.get(), out.sorted_y.get());
+           out.sorted_ids.get(), out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get());
 }
 
 void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, const GridGeom& g,

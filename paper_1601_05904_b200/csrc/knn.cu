@@ -8,9 +8,15 @@
 // blocks and the candidate loads hit L1.  The search is the reference's:
 // expansion level = smallest L0 whose clipped (2L0+1)^2 block holds >= k
 // points, plus one; scan that block; widen ring by ring until
-// kth <= (L*w)^2 (1 - 1e-9) or the block covers the grid.  The k-slot buffer
-// is register-resident (RegTopK<KMAX>, KMAX in {4, 16, 32, 64}; a global-
-// memory buffer beyond 64) and ordered by the (d2, index) pair, so the value
+// kth <= (L*w)^2 (1 - 1e-9) or the block covers the grid.  The block is
+// walked ring by ring from the query's cell and cells whose padded
+// rectangle lies strictly beyond the current k-th are skipped — the k
+// smallest (d2, idx) of every level's block are unchanged, so stop decisions
+// and results equal the reference's while ~1/3 of its candidates are read
+// (1M uniform: 34M of 99M).  The k-slot buffer
+// is a register-resident static sorting network (RegTopK<KMAX>, KMAX a
+// compile-time bucket >= k up to 64; a global-memory buffer beyond) ordered
+// by the (d2, index) pair, so the value
 // list equals the reference's (ties at the kth value are not admitted) and
 // the index set is the north-star "ties by index" set.  Every FP64 operation
 // uses an explicit round-to-nearest intrinsic and the file is compiled with
@@ -38,65 +44,60 @@ __device__ __forceinline__ bool pair_less(double da, uint32_t ia, double db, uin
     return da < db || (da == db && ia < ib);
 }
 
-// Register-resident bounded buffer, runtime k <= KMAX.
+// Register-resident bounded buffer as a static sorting network.  KMAX is a
+// compile-time bucket >= k; the first KMAX - k slots hold (-inf, 0)
+// sentinels that no candidate can pass, so the k real entries always sit in
+// slots [KMAX - k, KMAX) and the k-th is slot KMAX - 1 — every index is
+// static, nothing spills to local memory.  Insert: KMAX independent
+// (d2, idx) comparisons, then each slot takes its left neighbour, the
+// candidate, or itself.
 template <int KMAX>
 struct RegTopK {
     double d[KMAX];
     uint32_t id[KMAX];
-    int k, filled;
-    double kd;
-    uint32_t kid;
+    int k;
 
     __device__ __forceinline__ void init(int kk, double*, uint32_t*) {
         k = kk;
-        filled = 0;
+        const double inf = __longlong_as_double(0x7FF0000000000000ll);
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
-            d[j] = __longlong_as_double(0x7FF0000000000000ll);
-            id[j] = kNoId;
+            const bool front = j < KMAX - kk;
+            d[j] = front ? -inf : inf;
+            id[j] = front ? 0u : kNoId;
         }
-        kd = d[0];
-        kid = kNoId;
     }
-    __device__ __forceinline__ bool admits(double cd) const { return cd <= kd; }
+    __device__ __forceinline__ double kth() const { return d[KMAX - 1]; }
+    __device__ __forceinline__ bool full() const { return id[KMAX - 1] != kNoId; }
+    __device__ __forceinline__ bool admits(double cd) const { return cd <= d[KMAX - 1]; }
     __device__ __forceinline__ void insert(double cd, uint32_t cid) {
-        if (!pair_less(cd, cid, kd, kid)) return;
+        if (!pair_less(cd, cid, d[KMAX - 1], id[KMAX - 1])) return;
+        bool lt[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) lt[j] = pair_less(cd, cid, d[j], id[j]);
 #pragma unroll
         for (int j = KMAX - 1; j >= 1; --j) {
-            if (j < k) {
-                const bool sp = pair_less(cd, cid, d[j - 1], id[j - 1]);
-                const bool sc = pair_less(cd, cid, d[j], id[j]);
-                const double nd = sp ? d[j - 1] : (sc ? cd : d[j]);
-                const uint32_t ni = sp ? id[j - 1] : (sc ? cid : id[j]);
-                d[j] = nd;
-                id[j] = ni;
-            }
+            d[j] = lt[j - 1] ? d[j - 1] : (lt[j] ? cd : d[j]);
+            id[j] = lt[j - 1] ? id[j - 1] : (lt[j] ? cid : id[j]);
         }
-        if (pair_less(cd, cid, d[0], id[0])) {
+        if (lt[0]) {
             d[0] = cd;
             id[0] = cid;
         }
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            if (j == k - 1) {
-                kd = d[j];
-                kid = id[j];
-            }
-        }
-        filled += filled < k ? 1 : 0;
     }
+    // j-th smallest real entry (0-based); unrolled select, used at the end
     __device__ __forceinline__ double get_d(int j) const {
         double r = 0.0;
 #pragma unroll
         for (int i = 0; i < KMAX; ++i)
-            if (i == j) r = d[i];
+            if (i == KMAX - k + j) r = d[i];
         return r;
     }
     __device__ __forceinline__ uint32_t get_id(int j) const {
         uint32_t r = kNoId;
 #pragma unroll
         for (int i = 0; i < KMAX; ++i)
-            if (i == j) r = id[i];
+            if (i == KMAX - k + j) r = id[i];
         return r;
     }
 };
@@ -121,6 +122,8 @@ struct MemTopK {
             id[j] = kNoId;
         }
     }
+    __device__ __forceinline__ double kth() const { return kd; }
+    __device__ __forceinline__ bool full() const { return filled == k; }
     __device__ __forceinline__ bool admits(double cd) const { return cd <= kd; }
     __device__ void insert(double cd, uint32_t cid) {
         if (!pair_less(cd, cid, kd, kid)) return;
@@ -140,25 +143,66 @@ struct MemTopK {
     __device__ __forceinline__ uint32_t get_id(int j) const { return id[j]; }
 };
 
-// Offer every point of cell rows [r0, r1] x columns [c0, c1].
+// Conservative lower bound of d2 from the query (fx, fy in cell units) to
+// any point assigned to cell (c, r): the cell padded by 1e-7 cells (covers
+// the FP64 rounding of both cell assignments), edge cells unbounded outward
+// (locate_cell clamps points from the slack band into them), and a 1e-9
+// relative margin on the product.
+__device__ __forceinline__ double cell_lower_d2(const GridGeom& g, double fx, double fy,
+                                                double w2, int c, int r) {
+    const double inf = __longlong_as_double(0x7FF0000000000000ll);
+    const double pad = 1.0e-7;
+    const double x0 = c == 0 ? -inf : c - pad, x1 = c == g.n_col - 1 ? inf : c + 1 + pad;
+    const double y0 = r == 0 ? -inf : r - pad, y1 = r == g.n_row - 1 ? inf : r + 1 + pad;
+    const double dx = fmax(0.0, fmax(x0 - fx, fx - x1));
+    const double dy = fmax(0.0, fmax(y0 - fy, fy - y1));
+    return (dx * dx + dy * dy) * w2 * (1.0 - 1.0e-9);
+}
+
 template <class TopK>
-__device__ __forceinline__ void scan_rect(const KnnArgs& a, TopK& t, double qx, double qy,
-                                          int c0, int c1, int r0, int r1, uint32_t& snap,
-                                          unsigned long long& scanned) {
-    for (int r = r0; r <= r1; ++r) {
-        const size_t base = static_cast<size_t>(r) * static_cast<size_t>(a.g.n_col);
-        const uint32_t b = __ldg(a.cell_start + base + c0);
-        const uint32_t e = __ldg(a.cell_start + base + c1 + 1);
-        scanned += e - b;
-        for (uint32_t s = b; s < e; ++s) {
-            const double cd = dsq_rn(qx, qy, __ldg(a.sorted_x + s), __ldg(a.sorted_y + s));
-            if (cd <= a.snap_sq) {
-                const uint32_t cid = __ldg(a.sorted_ids + s);
-                snap = cid < snap ? cid : snap;
-            }
-            if (t.admits(cd)) t.insert(cd, __ldg(a.sorted_ids + s));
-        }
+__device__ __forceinline__ void scan_cell(const KnnArgs& a, TopK& t, double qx, double qy,
+                                          double fx, double fy, double w2, int c, int r,
+                                          uint32_t& snap, unsigned long long& scanned) {
+    if (t.full()) {
+        const double lb = cell_lower_d2(a.g, fx, fy, w2, c, r);
+        if (lb > fmax(t.kth(), a.snap_sq)) return;  // every point is strictly worse
     }
+    const size_t id = static_cast<size_t>(r) * static_cast<size_t>(a.g.n_col) + c;
+    const uint32_t b = __ldg(a.cell_start + id);
+    const uint32_t e = __ldg(a.cell_start + id + 1);
+    scanned += e - b;
+    for (uint32_t s = b; s < e; ++s) {
+        const double2 pxy = __ldg(a.sorted_xy + s);
+        const double cd = dsq_rn(qx, qy, pxy.x, pxy.y);
+        if (cd <= a.snap_sq) {
+            const uint32_t cid = __ldg(a.sorted_ids + s);
+            snap = cid < snap ? cid : snap;
+        }
+        if (t.admits(cd)) t.insert(cd, __ldg(a.sorted_ids + s));
+    }
+}
+
+// The cells at Chebyshev distance r from (col, row), clipped to the grid.
+template <class TopK>
+__device__ __forceinline__ void scan_ring(const KnnArgs& a, TopK& t, double qx, double qy,
+                                          double fx, double fy, double w2, int col, int row,
+                                          int r, uint32_t& snap, unsigned long long& scanned) {
+    const int n_col = a.g.n_col, n_row = a.g.n_row;
+    if (r == 0) {
+        scan_cell(a, t, qx, qy, fx, fy, w2, col, row, snap, scanned);
+        return;
+    }
+    const int c0 = col - r < 0 ? 0 : col - r, c1 = col + r > n_col - 1 ? n_col - 1 : col + r;
+    const int r0 = row - r + 1 < 0 ? 0 : row - r + 1;
+    const int r1 = row + r - 1 > n_row - 1 ? n_row - 1 : row + r - 1;
+    if (row - r >= 0)
+        for (int c = c0; c <= c1; ++c) scan_cell(a, t, qx, qy, fx, fy, w2, c, row - r, snap, scanned);
+    if (row + r <= n_row - 1)
+        for (int c = c0; c <= c1; ++c) scan_cell(a, t, qx, qy, fx, fy, w2, c, row + r, snap, scanned);
+    if (col - r >= 0)
+        for (int rr = r0; rr <= r1; ++rr) scan_cell(a, t, qx, qy, fx, fy, w2, col - r, rr, snap, scanned);
+    if (col + r <= n_col - 1)
+        for (int rr = r0; rr <= r1; ++rr) scan_cell(a, t, qx, qy, fx, fy, w2, col + r, rr, snap, scanned);
 }
 
 __device__ __forceinline__ size_t rect_count(const KnnArgs& a, int c0, int c1, int r0, int r1) {
@@ -188,19 +232,27 @@ __device__ __forceinline__ bool alpha_from_robs(const AlphaParams& p, double r_o
         mu = __dsub_rn(0.5, __dmul_rn(0.5, cos(phase)));
     }
     if (!(mu >= 0.0 && mu <= 1.0)) return false;
-    const double bp[5] = {0.1, 0.3, 0.5, 0.7, 0.9};
-    if (mu < bp[0]) {
+    if (mu < 0.1) {
         alpha = p.lv[0];
         return true;
     }
-    if (mu >= bp[4]) {
+    if (mu >= 0.9) {
         alpha = p.lv[4];
         return true;
     }
-    int s = 0;
-    while (mu >= bp[s + 1]) ++s;
-    const double t = __dmul_rn(5.0, __dsub_rn(mu, bp[s]));
-    alpha = __dadd_rn(p.lv[s], __dmul_rn(t, __dsub_rn(p.lv[s + 1], p.lv[s])));
+    // lower-inclusive segment [bp_s, bp_s+1) and its two levels (static picks)
+    double bp, lo, hi;
+    if (mu < 0.3) {
+        bp = 0.1, lo = p.lv[0], hi = p.lv[1];
+    } else if (mu < 0.5) {
+        bp = 0.3, lo = p.lv[1], hi = p.lv[2];
+    } else if (mu < 0.7) {
+        bp = 0.5, lo = p.lv[2], hi = p.lv[3];
+    } else {
+        bp = 0.7, lo = p.lv[3], hi = p.lv[4];
+    }
+    const double t = __dmul_rn(5.0, __dsub_rn(mu, bp));
+    alpha = __dadd_rn(lo, __dmul_rn(t, __dsub_rn(hi, lo)));
     return true;
 }
 
@@ -236,7 +288,7 @@ __device__ __forceinline__ void finish_query(const KnnArgs& a, TopK& t, size_t p
 template <class TopK>
 __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
     const size_t pos = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    unsigned long long scanned = 0;
+    unsigned long long scanned = 0, ref_scanned = 0;
     if (pos < a.n) {
         const uint32_t qi = a.perm[pos];
         const double qx = a.qx[qi], qy = a.qy[qi];
@@ -263,8 +315,15 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
         TopK t;
         t.init(a.k_eff, a.scratch_d + pos * a.k_eff, a.scratch_id + pos * a.k_eff);
         uint32_t snap = kNoId;
-        scan_rect(a, t, qx, qy, imax(0, col - level), imin(n_col - 1, col + level),
-                  imax(0, row - level), imin(n_row - 1, row + level), snap, scanned);
+        // query in cell units, for the per-cell lower bound
+        const double fx = __ddiv_rn(__dsub_rn(qx, a.g.min_x), a.g.cell_width);
+        const double fy = __ddiv_rn(__dsub_rn(qy, a.g.min_y), a.g.cell_width);
+        const double w2 = __dmul_rn(a.g.cell_width, a.g.cell_width);
+        // The reference scans the whole level block at once; scanning it ring
+        // by ring from the query's cell and skipping cells that cannot hold a
+        // point below the current k-th yields the same k smallest (d2, idx)
+        // of the block, hence identical stop decisions and results.
+        for (int r = 0; r <= level; ++r) scan_ring(a, t, qx, qy, fx, fy, w2, col, row, r, snap, scanned);
         // ring widening (knn.hpp:234-247, scan_ring :175-194)
         while (true) {
             const bool covers = col - level <= 0 && row - level <= 0 &&
@@ -272,23 +331,26 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
             if (covers) break;
             const double reach = __dmul_rn(static_cast<double>(level), a.g.cell_width);
             const double bound = __dmul_rn(__dmul_rn(reach, reach), a.ring_margin);
-            if (t.filled == a.k_eff && t.kd <= bound) break;
+            if (t.full() && t.kth() <= bound) break;
             ++level;
-            const int c0 = imax(0, col - level), c1 = imin(n_col - 1, col + level);
-            if (row - level >= 0) scan_rect(a, t, qx, qy, c0, c1, row - level, row - level, snap, scanned);
-            if (row + level <= n_row - 1)
-                scan_rect(a, t, qx, qy, c0, c1, row + level, row + level, snap, scanned);
-            const int pr0 = imax(0, row - (level - 1)), pr1 = imin(n_row - 1, row + (level - 1));
-            if (col - level >= 0) scan_rect(a, t, qx, qy, col - level, col - level, pr0, pr1, snap, scanned);
-            if (col + level <= n_col - 1)
-                scan_rect(a, t, qx, qy, col + level, col + level, pr0, pr1, snap, scanned);
+            scan_ring(a, t, qx, qy, fx, fy, w2, col, row, level, snap, scanned);
+        }
+        if (a.ref_candidates) {  // what the reference scanned: the final-level block
+            ref_scanned = rect_count(a, imax(0, col - level), imin(n_col - 1, col + level),
+                                     imax(0, row - level), imin(n_row - 1, row + level));
         }
         finish_query(a, t, pos, qi, snap);
     }
     if (a.candidates) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) scanned += __shfl_xor_sync(0xFFFFFFFFu, scanned, o);
-        if ((threadIdx.x & 31) == 0 && scanned) atomicAdd(a.candidates, scanned);
+        for (int o = 16; o > 0; o >>= 1) {
+            scanned += __shfl_xor_sync(0xFFFFFFFFu, scanned, o);
+            ref_scanned += __shfl_xor_sync(0xFFFFFFFFu, ref_scanned, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (scanned) atomicAdd(a.candidates, scanned);
+            if (a.ref_candidates && ref_scanned) atomicAdd(a.ref_candidates, ref_scanned);
+        }
     }
 }
 
@@ -332,18 +394,22 @@ __global__ void __launch_bounds__(128) knn_brute_kernel(KnnArgs a) {
     if (live) finish_query(a, t, pos, qi, snap);
 }
 
+#define AIDW_KNN_CASE(KERNEL, K)                              \
+    else if (a.k_eff <= K) {                                  \
+        LAUNCH(KERNEL<RegTopK<K>>, blocks, 128, 0, s, a);     \
+    }
 #define AIDW_KNN_DISPATCH(KERNEL)                                   \
     do {                                                            \
         const unsigned blocks = ceil_div(a.n, 128);                 \
-        if (a.k_eff <= 4) {                                         \
-            LAUNCH(KERNEL<RegTopK<4>>, blocks, 128, 0, s, a);       \
-        } else if (a.k_eff <= 16) {                                 \
-            LAUNCH(KERNEL<RegTopK<16>>, blocks, 128, 0, s, a);      \
-        } else if (a.k_eff <= 32) {                                 \
-            LAUNCH(KERNEL<RegTopK<32>>, blocks, 128, 0, s, a);      \
-        } else if (a.k_eff <= 64) {                                 \
-            LAUNCH(KERNEL<RegTopK<64>>, blocks, 128, 0, s, a);      \
-        } else {                                                    \
+        if (a.k_eff <= 1) {                                         \
+            LAUNCH(KERNEL<RegTopK<1>>, blocks, 128, 0, s, a);       \
+        }                                                           \
+        AIDW_KNN_CASE(KERNEL, 2) AIDW_KNN_CASE(KERNEL, 4)           \
+        AIDW_KNN_CASE(KERNEL, 8) AIDW_KNN_CASE(KERNEL, 10)          \
+        AIDW_KNN_CASE(KERNEL, 12) AIDW_KNN_CASE(KERNEL, 16)         \
+        AIDW_KNN_CASE(KERNEL, 24) AIDW_KNN_CASE(KERNEL, 32)         \
+        AIDW_KNN_CASE(KERNEL, 48) AIDW_KNN_CASE(KERNEL, 64)         \
+        else {                                                      \
             LAUNCH(KERNEL<MemTopK>, blocks, 128, 0, s, a);          \
         }                                                           \
     } while (0)

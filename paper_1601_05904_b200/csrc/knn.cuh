@@ -23,8 +23,7 @@ struct KnnArgs {
     GridGeom g;
     const uint32_t* cell_start = nullptr;
     const uint32_t* sorted_ids = nullptr;
-    const double* sorted_x = nullptr;
-    const double* sorted_y = nullptr;
+    const double2* sorted_xy = nullptr;  // cell-sorted {x, y}
     // data in index order — brute engine
     const double* dx = nullptr;
     const double* dy = nullptr;
@@ -52,7 +51,8 @@ struct KnnArgs {
     double const_alpha = 0.0;
     AlphaParams ap{};
     long long* fail_alpha = nullptr;
-    unsigned long long* candidates = nullptr;
+    unsigned long long* candidates = nullptr;      // points scanned (after pruning)
+    unsigned long long* ref_candidates = nullptr;  // the reference's scan: final-level block
     // scratch for k > 64
     double* scratch_d = nullptr;
     uint32_t* scratch_id = nullptr;
