@@ -245,6 +245,7 @@ enum { kFailData = 0, kFailQuery = 1, kFailAlpha = 2 };
 // stage ran (idw mode and the aidw_predict_all drop-in).  Uses a k = 1 grid
 // search (K1 + K2), or the brute kernel for tiny / degenerate sets.
 struct NearestInfo {
+    DeviceGrid grid;      // factor-4 grid (kept alive: its cell order feeds K4)
     DBuf<uint32_t> perm;  // visiting order
     DBuf<double> d2min;
     DBuf<uint32_t> nn, snap;
@@ -283,7 +284,7 @@ void nearest_search(const double* d_dx, const double* d_dy, size_t m, const doub
         run_knn_brute(a, s);
         return;
     }
-    DeviceGrid g;
+    DeviceGrid& g = out.grid;
     build_grid_device(d_dx, d_dy, m, cfg, g, fails.slot(kFailData), s);
     DBuf<uint32_t> qcell;
     const GridGeom geom = make_geom(cfg);
@@ -337,6 +338,7 @@ void weighting_stage(const double* d_dx, const double* d_dy, const double* d_dz,
     NearestInfo nb;
     nearest_search(d_dx, d_dy, m, d_qx, d_qy, n, ext.box, frame.snap_sq, nb, fails, s);
     const uint32_t* perm = nb.perm.n ? nb.perm.get() : nullptr;
+    wd.order = nb.grid.sorted_ids.n ? nb.grid.sorted_ids.get() : nullptr;
     DBuf<double> alpha_s(n, s);
     LAUNCH(gather_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_alpha_q, perm, n,
            alpha_s.get());
@@ -474,12 +476,12 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     knnb = ev.make();
     knne = ev.make();
 
+    DeviceGrid g;  // lives until the weighting stage has read its cell order
     if (cfg.engine == AIDW_ENGINE_GRID) {
         const double width = choose_cell_width_h(m, ext.box, cfg.cell_factor);
         const aidw_grid_config gc = make_grid_config_h(ext.box, width);
         validate_params(params);
         CK(cudaEventRecord(e_build0, s));
-        DeviceGrid g;
         build_grid_device(io.dx, io.dy, m, gc, g, fails.slot(kFailData), s);
         CK(cudaEventRecord(e_build1, s));
         const GridGeom geom = make_geom(gc);
@@ -507,6 +509,24 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     }
 
     WeightData wd{io.dx, io.dy, io.dz, m};
+    // K4 record order: cell order of the factor-4 grid over the bbox — the
+    // kNN grid when it is one, else built here — so the FP32 sums depend on
+    // the inputs only, never on the kNN engine or cell factor
+    DeviceGrid g4;
+    if (wmode == WeightMode::fp32 && m > 4096) {  // same rule as nearest_search
+        if (cfg.engine == AIDW_ENGINE_GRID && cfg.cell_factor == 4.0) {
+            wd.order = g.sorted_ids.get();
+        } else {
+            try {
+                const aidw_grid_config c4 =
+                    make_grid_config_h(ext.box, choose_cell_width_h(m, ext.box, 4.0));
+                build_grid_device(io.dx, io.dy, m, c4, g4, fails.slot(kFailData), s);
+                wd.order = g4.sorted_ids.get();
+            } catch (const Failure&) {
+                wd.order = nullptr;
+            }
+        }
+    }
     WeightQueries q;
     q.qx = io.qx;
     q.qy = io.qy;

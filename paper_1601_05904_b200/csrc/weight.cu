@@ -106,22 +106,50 @@ __device__ __forceinline__ void split_hilo(double v, float& hi, float& lo) {
     lo = __double2float_rn(v - static_cast<double>(hi));
 }
 
+// Record i = data point order[i] (cell order of the factor-4 grid, so a
+// 256-point tile is a compact strip of cells), or point i without order.
 __global__ void prep_data_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                 const double* __restrict__ z, size_t m, size_t mp, double ox,
-                                 double oy, double inv_scale, double zmul,
-                                 float4* __restrict__ xy, float* __restrict__ zz) {
+                                 const double* __restrict__ z, const uint32_t* __restrict__ order,
+                                 size_t m, size_t mp, double ox, double oy, double inv_scale,
+                                 double zmul, float4* __restrict__ xy, float* __restrict__ zz) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= mp) return;
     if (i < m) {
+        const size_t j = order ? order[i] : i;
         float xh, xl, yh, yl;
-        split_hilo((x[i] - ox) * inv_scale, xh, xl);
-        split_hilo((y[i] - oy) * inv_scale, yh, yl);
+        split_hilo((x[j] - ox) * inv_scale, xh, xl);
+        split_hilo((y[j] - oy) * inv_scale, yh, yl);
         xy[i] = make_float4(xh, yh, xl, yl);
-        zz[i] = __double2float_rn(z[i] * zmul);
+        zz[i] = __double2float_rn(z[j] * zmul);
     } else {
         xy[i] = make_float4(1.0e30f, 1.0e30f, 0.0f, 0.0f);
         zz[i] = 0.0f;
     }
+}
+
+// Bounding box (hi parts) of each 256-point tile's real records; one warp
+// per tile.  Drives the per-(query, tile) near / far choice in K4.
+__global__ void tile_box_kernel(const float4* __restrict__ xy, size_t m, size_t tiles,
+                                float4* __restrict__ box) {
+    const size_t tile = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (tile >= tiles) return;
+    float x0 = 3.0e38f, y0 = 3.0e38f, x1 = -3.0e38f, y1 = -3.0e38f;
+    for (int j = lane; j < kWeightTile; j += 32) {
+        const size_t i = tile * kWeightTile + j;
+        if (i < m) {
+            const float4 p = xy[i];
+            x0 = fminf(x0, p.x), y0 = fminf(y0, p.y), x1 = fmaxf(x1, p.x), y1 = fmaxf(y1, p.y);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        x0 = fminf(x0, __shfl_xor_sync(0xFFFFFFFFu, x0, o));
+        y0 = fminf(y0, __shfl_xor_sync(0xFFFFFFFFu, y0, o));
+        x1 = fmaxf(x1, __shfl_xor_sync(0xFFFFFFFFu, x1, o));
+        y1 = fmaxf(y1, __shfl_xor_sync(0xFFFFFFFFu, y1, o));
+    }
+    if (lane == 0) box[tile] = make_float4(x0, y0, x1, y1);
 }
 
 std::atomic<bool> g_alpha4_recipe{true};
@@ -181,6 +209,8 @@ struct K4Args {
     const float4* qpar;
     size_t n;
     double2* part;  // n * chunks
+    const float4* tile_box;  // hi-coordinate box of every tile's real records
+    float rfar2;             // squared near / far threshold (unit-box units)
 };
 
 // ---- packed f32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2): two queries per
@@ -223,62 +253,81 @@ struct QState {
     f2 xh[kPairs], yh[kPairs], xl[kPairs], yl[kPairs];
     f2 c[kPairs], b[kPairs], s[kPairs];
     bool a[QT];  // recipe class, per query
+    bool v[QT];  // query slot holds a real query
 };
 
-// One 256-point tile against the thread's kQT queries.  Per data point and
-// query pair: 3 FADD2 (dx), 3 FADD2 (dy), FMUL2 + FFMA2 (d2), then
+// One 256-point tile against the thread's QT queries.  Per data point and
+// query pair:
+//   NEAR tile (the query lies within R_far of the tile's box): hi/lo
+//     differences, dx = (x_hi - q_hi) + (x_lo - q_lo): 3 FADD2 each for dx, dy
+//   FAR tile: dx = x_hi - q_hi: 1 FADD2 each (relative error <= 6e-8 / R_far
+//     on pairs that carry a small share of the weight)
+//   d2 = dx dx + dy dy: FMUL2 + FFMA2, then
 //   MODE 3 (alpha == 4 recipe, s == 1): FMUL2 (d2^2), 2 x MUFU.RCP
 //   MODE 0 (alpha == 4 recipe, scaled): FMUL2 (d2 s), FMUL2 (^2), 2 x MUFU.RCP
 //   MODE 1 (general):           2 x MUFU.LG2, FFMA2 (c lg + b), 2 x MUFU.EX2
-//   MODE 2 (mixed warp):        per query, scalar, same roundings
-// and FADD2 (sum w) + FFMA2 (sum w z).
-template <int MODE, int QT>
+//   MODE 2 (mixed warp):        per query class and near flag, scalar, same roundings
+// and FADD2 (sum w) + FFMA2 (sum w z).  The formula is a function of the
+// (query, tile) pair only, so a query's result never depends on its warp.
+template <int MODE, bool NEAR, int QT>
 __device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
                                         const float* __restrict__ tz, const QState<QT>& q,
-                                        f2 (&sw)[QT / 2], f2 (&swz)[QT / 2]) {
+                                        const bool (&nq)[QT], f2 (&sw)[QT / 2],
+                                        f2 (&swz)[QT / 2]) {
     constexpr int kPairs = QT / 2;
 #pragma unroll 2
     for (int j = 0; j < kWeightTile; ++j) {
         const float4 p = txy[j];
         const float zz = tz[j];
-        const f2 px = pk2(p.x, p.x), py = pk2(p.y, p.y), pxl = pk2(p.z, p.z),
-                 pyl = pk2(p.w, p.w), pz = pk2(zz, zz);
+        const f2 px = pk2(p.x, p.x), py = pk2(p.y, p.y), pz = pk2(zz, zz);
 #pragma unroll
         for (int r = 0; r < kPairs; ++r) {
-            const f2 dx = add2(sub2(px, q.xh[r]), sub2(pxl, q.xl[r]));
-            const f2 dy = add2(sub2(py, q.yh[r]), sub2(pyl, q.yl[r]));
-            const f2 d2 = fma2(dx, dx, mul2(dy, dy));
             f2 w;
-            if (MODE == 3) {  // recipe, s == 1 for every query of the warp
-                float lo, hi;
-                up2(mul2(d2, d2), lo, hi);
-                w = pk2(mufu_rcp(lo), mufu_rcp(hi));
-            } else if (MODE == 0) {
-                const f2 t = mul2(d2, q.s[r]);
-                float lo, hi;
-                up2(mul2(t, t), lo, hi);
-                w = pk2(mufu_rcp(lo), mufu_rcp(hi));
-            } else if (MODE == 1) {
-                float lo, hi;
-                up2(d2, lo, hi);
-                up2(fma2(q.c[r], pk2(mufu_lg2(lo), mufu_lg2(hi)), q.b[r]), lo, hi);
-                w = pk2(mufu_ex2(lo), mufu_ex2(hi));
-            } else {
-                float d[2], cc[2], bb[2], ss[2], ww[2];
-                up2(d2, d[0], d[1]);
+            if (MODE == 2) {
+                float xh[2], yh[2], xl[2], yl[2], cc[2], bb[2], ss[2], ww[2];
+                up2(q.xh[r], xh[0], xh[1]);
+                up2(q.yh[r], yh[0], yh[1]);
+                up2(q.xl[r], xl[0], xl[1]);
+                up2(q.yl[r], yl[0], yl[1]);
                 up2(q.c[r], cc[0], cc[1]);
                 up2(q.b[r], bb[0], bb[1]);
                 up2(q.s[r], ss[0], ss[1]);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
+                    float dx = p.x - xh[h], dy = p.y - yh[h];
+                    if (nq[2 * r + h]) {
+                        dx = dx + (p.z - xl[h]);
+                        dy = dy + (p.w - yl[h]);
+                    }
+                    const float d2 = fmaf(dx, dx, dy * dy);
                     if (q.a[2 * r + h]) {
-                        const float t = d[h] * ss[h];
+                        const float t = d2 * ss[h];
                         ww[h] = mufu_rcp(t * t);
                     } else {
-                        ww[h] = mufu_ex2(fmaf(cc[h], mufu_lg2(d[h]), bb[h]));
+                        ww[h] = mufu_ex2(fmaf(cc[h], mufu_lg2(d2), bb[h]));
                     }
                 }
                 w = pk2(ww[0], ww[1]);
+            } else {
+                f2 dx = sub2(px, q.xh[r]), dy = sub2(py, q.yh[r]);
+                if (NEAR) {
+                    dx = add2(dx, sub2(pk2(p.z, p.z), q.xl[r]));
+                    dy = add2(dy, sub2(pk2(p.w, p.w), q.yl[r]));
+                }
+                const f2 d2 = fma2(dx, dx, mul2(dy, dy));
+                float lo, hi;
+                if (MODE == 3) {  // recipe, s == 1 for every query of the warp
+                    up2(mul2(d2, d2), lo, hi);
+                    w = pk2(mufu_rcp(lo), mufu_rcp(hi));
+                } else if (MODE == 0) {
+                    const f2 t = mul2(d2, q.s[r]);
+                    up2(mul2(t, t), lo, hi);
+                    w = pk2(mufu_rcp(lo), mufu_rcp(hi));
+                } else {
+                    up2(d2, lo, hi);
+                    up2(fma2(q.c[r], pk2(mufu_lg2(lo), mufu_lg2(hi)), q.b[r]), lo, hi);
+                    w = pk2(mufu_ex2(lo), mufu_ex2(hi));
+                }
             }
             sw[r] = add2(sw[r], w);
             swz[r] = fma2(w, pz, swz[r]);
@@ -315,11 +364,13 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
                 h[i] = a.qhl[p];
                 r[i] = a.qpar[p];
                 q.a[i] = r[i].w != 0.0f;
+                q.v[i] = true;
                 any_a |= q.a[i];
                 any_g |= !q.a[i];
                 any_scaled |= r[i].z != 1.0f;
             } else {
                 q.a[i] = true;
+                q.v[i] = false;
             }
         }
 #pragma unroll
@@ -368,14 +419,40 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
         f2 sw[kPairs], swz[kPairs];
 #pragma unroll
         for (int k = 0; k < kPairs; ++k) sw[k] = swz[k] = 0ull;
-        if (mode == 3) {
-            k4_tile<3, kQT>(txy, tz, q, sw, swz);
-        } else if (mode == 0) {
-            k4_tile<0, kQT>(txy, tz, q, sw, swz);
-        } else if (mode == 1) {
-            k4_tile<1, kQT>(txy, tz, q, sw, swz);
+        // per-(query, tile) near flags, then a warp-uniform dispatch
+        const float4 tb = __ldg(a.tile_box + t0 + it);
+        bool nq[kQT];
+        bool any_near = false, all_near = true;
+#pragma unroll
+        for (int k = 0; k < kPairs; ++k) {
+            float x[2], y[2];
+            up2(q.xh[k], x[0], x[1]);
+            up2(q.yh[k], y[0], y[1]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float ex = fmaxf(0.0f, fmaxf(tb.x - x[h], x[h] - tb.z));
+                const float ey = fmaxf(0.0f, fmaxf(tb.y - y[h], y[h] - tb.w));
+                nq[2 * k + h] = fmaf(ex, ex, ey * ey) <= a.rfar2;
+                if (q.v[2 * k + h]) {  // empty slots never force a mixed tile
+                    any_near |= nq[2 * k + h];
+                    all_near &= nq[2 * k + h];
+                }
+            }
+        }
+        any_near = __any_sync(0xFFFFFFFFu, any_near);
+        all_near = __all_sync(0xFFFFFFFFu, all_near);
+        const int tmode = (!any_near || all_near) ? mode : 2;
+        if (tmode == 3) {
+            if (any_near) k4_tile<3, true, kQT>(txy, tz, q, nq, sw, swz);
+            else k4_tile<3, false, kQT>(txy, tz, q, nq, sw, swz);
+        } else if (tmode == 0) {
+            if (any_near) k4_tile<0, true, kQT>(txy, tz, q, nq, sw, swz);
+            else k4_tile<0, false, kQT>(txy, tz, q, nq, sw, swz);
+        } else if (tmode == 1) {
+            if (any_near) k4_tile<1, true, kQT>(txy, tz, q, nq, sw, swz);
+            else k4_tile<1, false, kQT>(txy, tz, q, nq, sw, swz);
         } else {
-            k4_tile<2, kQT>(txy, tz, q, sw, swz);
+            k4_tile<2, true, kQT>(txy, tz, q, nq, sw, swz);
         }
 #pragma unroll
         for (int k = 0; k < kPairs; ++k) {
@@ -463,10 +540,12 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     if (q.n == 0) return;
     const WeightSplit sp = weight_split(d.m);
     const size_t mp = sp.tiles * kWeightTile;
-    DBuf<float4> xy(mp, s);
+    DBuf<float4> xy(mp, s), tbox(sp.tiles, s);
     DBuf<float> zz(mp, s);
-    LAUNCH(prep_data_kernel, ceil_div(mp, kThreads), kThreads, 0, s, d.x, d.y, d.z, d.m, mp,
-           f.ox, f.oy, f.inv_scale, std::ldexp(1.0, f.zshift), xy.get(), zz.get());
+    LAUNCH(prep_data_kernel, ceil_div(mp, kThreads), kThreads, 0, s, d.x, d.y, d.z, d.order, d.m,
+           mp, f.ox, f.oy, f.inv_scale, std::ldexp(1.0, f.zshift), xy.get(), zz.get());
+    LAUNCH(tile_box_kernel, ceil_div(sp.tiles * 32, kThreads), kThreads, 0, s, xy.get(), d.m,
+           sp.tiles, tbox.get());
 
     DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), order(q.n, s);
     DBuf<float4> qhl(q.n, s), qpar(q.n, s);
@@ -479,12 +558,18 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
            times ? times->d_alpha4 : nullptr);
 
     DBuf<double2> part(q.n * sp.chunks, s);
+    // near / far threshold (unit-box units): beyond it a pair's plain FP32
+    // difference has relative error <= ~8.4e-8 / R_far (AIDW_K4_RFAR to tune)
+    static const float rfar = [] {
+        const char* v = std::getenv("AIDW_K4_RFAR");
+        return v ? static_cast<float>(std::atof(v)) : 0.05f;
+    }();
     K4Args ka{xy.get(), zz.get(), sp.tiles, sp.tiles_per_chunk, sp.chunks, qhl.get(), qpar.get(),
-              q.n, part.get()};
+              q.n, part.get(), tbox.get(), rfar * rfar};
     const size_t smem = kStages * kWeightTile * (sizeof(float4) + sizeof(float)) +
                         kStages * sizeof(uint64_t);
     // K4 variant: queries per thread x min resident CTAs (AIDW_K4_VARIANT for
-    // tuning; default 4x2).  Per-query arithmetic is identical in all.
+    // tuning; default 4 x 3).  Per-query arithmetic is identical in all.
     static const int variant = [] {
         const char* v = std::getenv("AIDW_K4_VARIANT");
         return v ? std::atoi(v) : 0;
@@ -497,14 +582,8 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
         LAUNCH(kernel, grid, kK4Threads, smem, s, ka);
     };
     switch (variant) {
-        case 1: launch(weight_fp32_kernel<8, 1>, 8); break;
-        case 2: launch(weight_fp32_kernel<4, 3>, 4); break;
-        case 3: launch(weight_fp32_kernel<2, 3>, 2); break;
-        case 4: launch(weight_fp32_kernel<8, 2>, 8); break;
-        case 5: launch(weight_fp32_kernel<4, 4>, 4); break;
-        case 6: launch(weight_fp32_kernel<2, 4>, 2); break;
-        case 7: launch(weight_fp32_kernel<6, 2>, 6); break;
-        case 8: launch(weight_fp32_kernel<4, 2>, 4); break;
+        case 1: launch(weight_fp32_kernel<4, 2>, 4); break;
+        case 2: launch(weight_fp32_kernel<2, 4>, 2); break;
         default: launch(weight_fp32_kernel<4, 3>, 4); break;
     }
     if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));

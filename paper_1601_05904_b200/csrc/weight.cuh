@@ -36,6 +36,9 @@ struct WeightData {
     const double* y = nullptr;
     const double* z = nullptr;
     size_t m = 0;
+    // FP32 path: record order (cell order of the factor-4 grid over the
+    // bbox, so tiles are spatially compact); nullptr = index order
+    const uint32_t* order = nullptr;
 };
 
 // Optional instrumentation: events recorded around the K4 launch(es) and a
