@@ -302,6 +302,10 @@ def main():
     build_ms = statistics.median(s["build_ms"] for s in stats)
     build_bytes = 64 * m + 8 * (m // 4 + 1)  # factor-4 grid: ~m/4 cells (SURVEY §8 grid table)
     a4 = stats[-1]["alpha4_queries"]
+    # MUFU ops per pair of the executed formula mix: 1 (rcp) for queries on
+    # the exact alpha = 4 recipe, 2 (lg2 + ex2) for every other query
+    mufu_per_pair = (a4 * 1 + (n - a4) * 2) / n
+    peak_mix = sms * 16 * f_mhz * 1e6 / mufu_per_pair / 1e9
 
     # general-alpha path forced (every query on exp2/log2), reported separately
     A.set_alpha4_recipe(False)
@@ -348,10 +352,13 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write)",
                        "device": name, "sms": sms},
             "roofline": {"bound": "mufu", "kernel": "weight_fp32_kernel (K4)",
-                         "achieved": achieved, "peak": peak_gpairs, "unit": "Gpair/s",
-                         "frac": achieved / peak_gpairs, "traffic": None,
-                         "peak_def": f"{sms} SMs x 16 MUFU/clk / 2 MUFU per pair x "
-                                     f"{f_mhz:.0f} MHz ({pk['source']} sm_max_mhz)",
+                         "achieved": achieved, "peak": peak_mix, "unit": "Gpair/s",
+                         "frac": achieved / peak_mix, "traffic": None,
+                         "peak_def": f"{sms} SMs x 16 MUFU/clk x {f_mhz:.0f} MHz ({pk['source']} "
+                                     f"sm_max_mhz) / {mufu_per_pair:.4f} MUFU per pair (executed "
+                                     f"mix: 1 for alpha=4 recipe queries, 2 for exp2/log2)",
+                         "mufu_per_pair": mufu_per_pair,
+                         "frac_vs_2mufu_roofline": achieved / peak_gpairs,
                          "alpha4_recipe_queries": a4, "pairs_per_launch": pairs,
                          "k4_ms": k4_ms},
             "roofline_general_alpha": {"bound": "mufu", "achieved": pairs / (k4g_ms / 1e3) / 1e9,
