@@ -190,7 +190,10 @@ struct Events {
     }
     static double ms(cudaEvent_t a, cudaEvent_t b) {
         float t = 0.f;
-        if (a && b && cudaEventElapsedTime(&t, a, b) == cudaSuccess) return t;
+        if (a && b) {
+            if (cudaEventElapsedTime(&t, a, b) == cudaSuccess) return t;
+            cudaGetLastError();  // stage never ran (e.g. n == 0): clear, do not leak
+        }
         return 0.0;
     }
     ~Events() {
@@ -365,6 +368,7 @@ void fill_error(aidw_error* err, int code, const std::string& msg, long long ind
 template <class F>
 int guarded(aidw_error* err, F&& body) {
     if (err) fill_error(err, AIDW_OK, "", -1);
+    cudaGetLastError();  // our static runtime: drop any stale error from an earlier call
     try {
         body();
         return AIDW_OK;

@@ -111,7 +111,7 @@ __device__ __forceinline__ void split_hilo(double v, float& hi, float& lo) {
 __global__ void prep_data_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                  const double* __restrict__ z, const uint32_t* __restrict__ order,
                                  size_t m, size_t mp, double ox, double oy, double inv_scale,
-                                 double zmul, float4* __restrict__ xy, float* __restrict__ zz) {
+                                 double zmul, float4* __restrict__ xy, float2* __restrict__ zz) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= mp) return;
     if (i < m) {
@@ -120,10 +120,12 @@ __global__ void prep_data_kernel(const double* __restrict__ x, const double* __r
         split_hilo((x[j] - ox) * inv_scale, xh, xl);
         split_hilo((y[j] - oy) * inv_scale, yh, yl);
         xy[i] = make_float4(xh, yh, xl, yl);
-        zz[i] = __double2float_rn(z[j] * zmul);
+        float zh, zl;
+        split_hilo(z[j] * zmul, zh, zl);
+        zz[i] = make_float2(zh, zl);
     } else {
         xy[i] = make_float4(1.0e30f, 1.0e30f, 0.0f, 0.0f);
-        zz[i] = 0.0f;
+        zz[i] = make_float2(0.0f, 0.0f);
     }
 }
 
@@ -202,7 +204,7 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
 // ------------------------------------------------------------ K4
 struct K4Args {
     const float4* xy;
-    const float* z;
+    const float2* z;  // {z_hi, z_lo} scaled values
     size_t tiles, tiles_per_chunk;
     unsigned chunks;
     const float4* qhl;
@@ -266,20 +268,30 @@ struct QState {
 //   MODE 3 (alpha == 4 recipe, s == 1): FMUL2 (d2^2), 2 x MUFU.RCP
 //   MODE 0 (alpha == 4 recipe, scaled): FMUL2 (d2 s), FMUL2 (^2), 2 x MUFU.RCP
 //   MODE 1 (general):           2 x MUFU.LG2, FFMA2 (c lg + b), 2 x MUFU.EX2
-//   MODE 2 (mixed warp):        per query class and near flag, scalar, same roundings
-// and FADD2 (sum w) + FFMA2 (sum w z).  The formula is a function of the
-// (query, tile) pair only, so a query's result never depends on its warp.
-template <int MODE, bool NEAR, int QT>
+//   MODE 2 (mixed class warp):  per query class and near flag, scalar, same roundings
+// and FADD2 (sum w) + FFMA2 (sum w z) — Kahan-compensated with hi/lo z in
+// NEAR tiles, where a query's large terms live.  DIST: 0 = every query of
+// the warp far, 1 = every query near, 2 = mixed (both forms, per-lane
+// select).  The formula is a function of the (query, tile) pair only, so a
+// query's result never depends on its warp or lane.
+__device__ __forceinline__ f2 sel2(f2 a, f2 b, bool take_a_lo, bool take_a_hi) {
+    float alo, ahi, blo, bhi;
+    up2(a, alo, ahi);
+    up2(b, blo, bhi);
+    return pk2(take_a_lo ? alo : blo, take_a_hi ? ahi : bhi);
+}
+
+template <int MODE, int DIST, int QT>
 __device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
-                                        const float* __restrict__ tz, const QState<QT>& q,
+                                        const float2* __restrict__ tz, const QState<QT>& q,
                                         const bool (&nq)[QT], f2 (&sw)[QT / 2],
-                                        f2 (&swz)[QT / 2]) {
+                                        f2 (&swz)[QT / 2], f2 (&cz)[QT / 2]) {
     constexpr int kPairs = QT / 2;
 #pragma unroll 2
     for (int j = 0; j < kWeightTile; ++j) {
         const float4 p = txy[j];
-        const float zz = tz[j];
-        const f2 px = pk2(p.x, p.x), py = pk2(p.y, p.y), pz = pk2(zz, zz);
+        const float2 zz = tz[j];
+        const f2 px = pk2(p.x, p.x), py = pk2(p.y, p.y), pz = pk2(zz.x, zz.x);
 #pragma unroll
         for (int r = 0; r < kPairs; ++r) {
             f2 w;
@@ -310,9 +322,12 @@ __device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
                 w = pk2(ww[0], ww[1]);
             } else {
                 f2 dx = sub2(px, q.xh[r]), dy = sub2(py, q.yh[r]);
-                if (NEAR) {
+                if (DIST == 1) {
                     dx = add2(dx, sub2(pk2(p.z, p.z), q.xl[r]));
                     dy = add2(dy, sub2(pk2(p.w, p.w), q.yl[r]));
+                } else if (DIST == 2) {
+                    dx = sel2(add2(dx, sub2(pk2(p.z, p.z), q.xl[r])), dx, nq[2 * r], nq[2 * r + 1]);
+                    dy = sel2(add2(dy, sub2(pk2(p.w, p.w), q.yl[r])), dy, nq[2 * r], nq[2 * r + 1]);
                 }
                 const f2 d2 = fma2(dx, dx, mul2(dy, dy));
                 float lo, hi;
@@ -330,7 +345,40 @@ __device__ __forceinline__ void k4_tile(const float4* __restrict__ txy,
                 }
             }
             sw[r] = add2(sw[r], w);
-            swz[r] = fma2(w, pz, swz[r]);
+            if (MODE == 2) {  // per query: compensated when near, plain when far
+                float wv[2], sv[2], cv[2];
+                up2(w, wv[0], wv[1]);
+                up2(swz[r], sv[0], sv[1]);
+                up2(cz[r], cv[0], cv[1]);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (nq[2 * r + h]) {
+                        const float t = fmaf(wv[h], zz.x, wv[h] * zz.y);
+                        const float y = t - cv[h];
+                        const float s2 = sv[h] + y;
+                        cv[h] = (s2 - sv[h]) - y;
+                        sv[h] = s2;
+                    } else {
+                        sv[h] = fmaf(wv[h], zz.x, sv[h]);
+                    }
+                }
+                swz[r] = pk2(sv[0], sv[1]);
+                cz[r] = pk2(cv[0], cv[1]);
+            } else if (DIST == 0) {
+                swz[r] = fma2(w, pz, swz[r]);
+            } else {  // Kahan-compensated w z with hi/lo z
+                const f2 t = fma2(w, pz, mul2(w, pk2(zz.y, zz.y)));
+                const f2 y = sub2(t, cz[r]);
+                const f2 s2 = add2(swz[r], y);
+                const f2 c2 = sub2(sub2(s2, swz[r]), y);
+                if (DIST == 1) {
+                    cz[r] = c2;
+                    swz[r] = s2;
+                } else {
+                    cz[r] = sel2(c2, cz[r], nq[2 * r], nq[2 * r + 1]);
+                    swz[r] = sel2(s2, fma2(w, pz, swz[r]), nq[2 * r], nq[2 * r + 1]);
+                }
+            }
         }
     }
 }
@@ -340,7 +388,7 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
     constexpr int kPairs = kQT / 2;
     extern __shared__ __align__(128) unsigned char smem[];
     float4* sxy = reinterpret_cast<float4*>(smem);
-    float* sz = reinterpret_cast<float*>(sxy + kStages * kWeightTile);
+    float2* sz = reinterpret_cast<float2*>(sxy + kStages * kWeightTile);
     uint64_t* bar = reinterpret_cast<uint64_t*>(sz + kStages * kWeightTile);
 
     const unsigned chunk = blockIdx.y;
@@ -398,7 +446,7 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
     for (int i = 0; i < kQT; ++i) SW[i] = SWZ[i] = 0.0;
 
     constexpr uint32_t kXYBytes = kWeightTile * sizeof(float4);
-    constexpr uint32_t kZBytes = kWeightTile * sizeof(float);
+    constexpr uint32_t kZBytes = kWeightTile * sizeof(float2);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
@@ -415,10 +463,10 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
         const int st = static_cast<int>(it % kStages);
         mbar_wait(&bar[st], static_cast<uint32_t>((it / kStages) & 1));
         const float4* txy = sxy + st * kWeightTile;
-        const float* tz = sz + st * kWeightTile;
-        f2 sw[kPairs], swz[kPairs];
+        const float2* tz = sz + st * kWeightTile;
+        f2 sw[kPairs], swz[kPairs], cz[kPairs];
 #pragma unroll
-        for (int k = 0; k < kPairs; ++k) sw[k] = swz[k] = 0ull;
+        for (int k = 0; k < kPairs; ++k) sw[k] = swz[k] = cz[k] = 0ull;
         // per-(query, tile) near flags, then a warp-uniform dispatch
         const float4 tb = __ldg(a.tile_box + t0 + it);
         bool nq[kQT];
@@ -441,18 +489,20 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
         }
         any_near = __any_sync(0xFFFFFFFFu, any_near);
         all_near = __all_sync(0xFFFFFFFFu, all_near);
-        const int tmode = (!any_near || all_near) ? mode : 2;
-        if (tmode == 3) {
-            if (any_near) k4_tile<3, true, kQT>(txy, tz, q, nq, sw, swz);
-            else k4_tile<3, false, kQT>(txy, tz, q, nq, sw, swz);
-        } else if (tmode == 0) {
-            if (any_near) k4_tile<0, true, kQT>(txy, tz, q, nq, sw, swz);
-            else k4_tile<0, false, kQT>(txy, tz, q, nq, sw, swz);
-        } else if (tmode == 1) {
-            if (any_near) k4_tile<1, true, kQT>(txy, tz, q, nq, sw, swz);
-            else k4_tile<1, false, kQT>(txy, tz, q, nq, sw, swz);
+        const int dist = !any_near ? 0 : (all_near ? 1 : 2);
+        if (mode == 3) {
+            if (dist == 0) k4_tile<3, 0, kQT>(txy, tz, q, nq, sw, swz, cz);
+            else if (dist == 1) k4_tile<3, 1, kQT>(txy, tz, q, nq, sw, swz, cz);
+            else k4_tile<3, 2, kQT>(txy, tz, q, nq, sw, swz, cz);
+        } else if (mode == 0) {
+            if (dist == 0) k4_tile<0, 0, kQT>(txy, tz, q, nq, sw, swz, cz);
+            else k4_tile<0, 2, kQT>(txy, tz, q, nq, sw, swz, cz);
+        } else if (mode == 1) {
+            if (dist == 0) k4_tile<1, 0, kQT>(txy, tz, q, nq, sw, swz, cz);
+            else if (dist == 1) k4_tile<1, 1, kQT>(txy, tz, q, nq, sw, swz, cz);
+            else k4_tile<1, 2, kQT>(txy, tz, q, nq, sw, swz, cz);
         } else {
-            k4_tile<2, true, kQT>(txy, tz, q, nq, sw, swz);
+            k4_tile<2, 2, kQT>(txy, tz, q, nq, sw, swz, cz);
         }
 #pragma unroll
         for (int k = 0; k < kPairs; ++k) {
@@ -461,8 +511,10 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
             SW[2 * k] += static_cast<double>(lo);
             SW[2 * k + 1] += static_cast<double>(hi);
             up2(swz[k], lo, hi);
-            SWZ[2 * k] += static_cast<double>(lo);
-            SWZ[2 * k + 1] += static_cast<double>(hi);
+            float clo, chi;
+            up2(cz[k], clo, chi);
+            SWZ[2 * k] += static_cast<double>(lo) - static_cast<double>(clo);
+            SWZ[2 * k + 1] += static_cast<double>(hi) - static_cast<double>(chi);
         }
         __syncthreads();
         if (threadIdx.x == 0 && it + kStages < ntl) {
@@ -541,7 +593,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     const WeightSplit sp = weight_split(d.m);
     const size_t mp = sp.tiles * kWeightTile;
     DBuf<float4> xy(mp, s), tbox(sp.tiles, s);
-    DBuf<float> zz(mp, s);
+    DBuf<float2> zz(mp, s);
     LAUNCH(prep_data_kernel, ceil_div(mp, kThreads), kThreads, 0, s, d.x, d.y, d.z, d.order, d.m,
            mp, f.ox, f.oy, f.inv_scale, std::ldexp(1.0, f.zshift), xy.get(), zz.get());
     LAUNCH(tile_box_kernel, ceil_div(sp.tiles * 32, kThreads), kThreads, 0, s, xy.get(), d.m,
@@ -566,7 +618,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     }();
     K4Args ka{xy.get(), zz.get(), sp.tiles, sp.tiles_per_chunk, sp.chunks, qhl.get(), qpar.get(),
               q.n, part.get(), tbox.get(), rfar * rfar};
-    const size_t smem = kStages * kWeightTile * (sizeof(float4) + sizeof(float)) +
+    const size_t smem = kStages * kWeightTile * (sizeof(float4) + sizeof(float2)) +
                         kStages * sizeof(uint64_t);
     // K4 variant: queries per thread x min resident CTAs (AIDW_K4_VARIANT for
     // tuning; default 4 x 3).  Per-query arithmetic is identical in all.
