@@ -55,6 +55,19 @@ def peaks():
     return p
 
 
+def k4_traffic(cfg):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one K4 launch from the
+    latest committed `ncu --set full` capture of the bench config (or None)."""
+    import glob
+    if cfg is not CONFIGS["1m"]:
+        return None
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k4_traffic.json")))
+    if not paths:
+        return None
+    with open(paths[-1]) as f:
+        return json.load(f).get("dram_bytes_per_launch")
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -353,7 +366,7 @@ def main():
                        "device": name, "sms": sms},
             "roofline": {"bound": "mufu", "kernel": "weight_fp32_kernel (K4)",
                          "achieved": achieved, "peak": peak_mix, "unit": "Gpair/s",
-                         "frac": achieved / peak_mix, "traffic": None,
+                         "frac": achieved / peak_mix, "traffic": k4_traffic(cfg),
                          "peak_def": f"{sms} SMs x 16 MUFU/clk x {f_mhz:.0f} MHz ({pk['source']} "
                                      f"sm_max_mhz) / {mufu_per_pair:.4f} MUFU per pair (executed "
                                      f"mix: 1 for alpha=4 recipe queries, 2 for exp2/log2)",
