@@ -322,6 +322,13 @@ WeightMode weight_mode(int32_t variant, int32_t pinned) {
 }
 
 // Weighting stage over device-resident inputs given alpha by query index.
+void set_order(WeightData& wd, const DeviceGrid& g) {
+    wd.order = g.sorted_ids.get();
+    wd.cell_start = g.cell_start.get();
+    wd.n_col = g.cfg.n_col;
+    wd.n_row = g.cfg.n_row;
+}
+
 // d_alpha_q: alpha per query (input order).
 void weighting_stage(const double* d_dx, const double* d_dy, const double* d_dz, size_t m,
                      const double* d_qx, const double* d_qy, size_t n, const double* d_alpha_q,
@@ -341,7 +348,7 @@ void weighting_stage(const double* d_dx, const double* d_dy, const double* d_dz,
     NearestInfo nb;
     nearest_search(d_dx, d_dy, m, d_qx, d_qy, n, ext.box, frame.snap_sq, nb, fails, s);
     const uint32_t* perm = nb.perm.n ? nb.perm.get() : nullptr;
-    wd.order = nb.grid.sorted_ids.n ? nb.grid.sorted_ids.get() : nullptr;
+    if (nb.grid.sorted_ids.n) set_order(wd, nb.grid);
     DBuf<double> alpha_s(n, s);
     LAUNCH(gather_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_alpha_q, perm, n,
            alpha_s.get());
@@ -519,13 +526,13 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     DeviceGrid g4;
     if (wmode == WeightMode::fp32 && m > 4096) {  // same rule as nearest_search
         if (cfg.engine == AIDW_ENGINE_GRID && cfg.cell_factor == 4.0) {
-            wd.order = g.sorted_ids.get();
+            set_order(wd, g);
         } else {
             try {
                 const aidw_grid_config c4 =
                     make_grid_config_h(ext.box, choose_cell_width_h(m, ext.box, 4.0));
                 build_grid_device(io.dx, io.dy, m, c4, g4, fails.slot(kFailData), s);
-                wd.order = g4.sorted_ids.get();
+                set_order(wd, g4);
             } catch (const Failure&) {
                 wd.order = nullptr;
             }

@@ -139,6 +139,11 @@ struct DeviceGrid {
     DBuf<double2> sorted_xy;          // interleaved copy the kNN kernel reads
 };
 
+// order[0..m) = the grid's point ids with cells visited in 8 x 8-cell blocks
+// (blocks row-major, cells row-major inside): compact K4 data tiles.
+void blocked_cell_order(const uint32_t* d_cell_start, const uint32_t* d_sorted_ids, int n_col,
+                        int n_row, size_t m, uint32_t* d_order, cudaStream_t s);
+
 // Builds the CSR grid from device x/y (m points).  Out-of-region points
 // set *d_fail (atomicMin of the point index); the caller checks it.
 void build_grid_device(const double* d_x, const double* d_y, size_t m,

@@ -281,6 +281,43 @@ __global__ void decode_minmax_kernel(const unsigned long long* __restrict__ keys
     }
 }
 
+// Blocked cell order (K4 data tiles): cells visited in 8 x 8-cell blocks,
+// blocks row-major, cells row-major inside a block.  On a factor-4 grid a
+// block holds ~256 points (16 r_exp^2 m / A = 4 points per cell), so a
+// 256-record K4 tile is a compact square instead of a 64-cell strip.
+constexpr int kOrderBlock = 8;
+
+__device__ __forceinline__ bool block_slot_cell(size_t j, int n_col, int n_row, unsigned nbc,
+                                                size_t& cell) {
+    const size_t b = j / (kOrderBlock * kOrderBlock);
+    const int w = static_cast<int>(j % (kOrderBlock * kOrderBlock));
+    const size_t row = (b / nbc) * kOrderBlock + w / kOrderBlock;
+    const size_t col = (b % nbc) * kOrderBlock + w % kOrderBlock;
+    if (row >= static_cast<size_t>(n_row) || col >= static_cast<size_t>(n_col)) return false;
+    cell = row * static_cast<size_t>(n_col) + col;
+    return true;
+}
+
+__global__ void block_counts_kernel(const uint32_t* __restrict__ cell_start, int n_col, int n_row,
+                                    unsigned nbc, size_t slots, uint32_t* __restrict__ cnt) {
+    const size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= slots) return;
+    size_t c;
+    cnt[j] = block_slot_cell(j, n_col, n_row, nbc, c) ? cell_start[c + 1] - cell_start[c] : 0u;
+}
+
+__global__ void block_scatter_kernel(const uint32_t* __restrict__ cell_start,
+                                     const uint32_t* __restrict__ sorted_ids, int n_col, int n_row,
+                                     unsigned nbc, size_t slots, const uint32_t* __restrict__ start,
+                                     uint32_t* __restrict__ order) {
+    const size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= slots) return;
+    size_t c;
+    if (!block_slot_cell(j, n_col, n_row, nbc, c)) return;
+    const uint32_t b = cell_start[c], e = cell_start[c + 1], o = start[j];
+    for (uint32_t t = b; t < e; ++t) order[o + (t - b)] = sorted_ids[t];
+}
+
 int bits_for(uint64_t max_key) {
     int b = 0;
     while (b < 32 && (max_key >> b) != 0) ++b;
@@ -321,6 +358,20 @@ void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaSt
         CK(cudaMemcpyAsync(keys, ki, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(vals, vi, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     }
+}
+
+void blocked_cell_order(const uint32_t* d_cell_start, const uint32_t* d_sorted_ids, int n_col,
+                        int n_row, size_t m, uint32_t* d_order, cudaStream_t s) {
+    if (m == 0) return;
+    const unsigned nbc = static_cast<unsigned>((n_col + kOrderBlock - 1) / kOrderBlock);
+    const size_t nbr = static_cast<size_t>((n_row + kOrderBlock - 1) / kOrderBlock);
+    const size_t slots = nbr * nbc * kOrderBlock * kOrderBlock;
+    DBuf<uint32_t> cnt(slots, s);
+    LAUNCH(block_counts_kernel, ceil_div(slots, kThreads), kThreads, 0, s, d_cell_start, n_col,
+           n_row, nbc, slots, cnt.get());
+    exclusive_scan_u32(cnt.get(), cnt.get(), slots, s);
+    LAUNCH(block_scatter_kernel, ceil_div(slots, kThreads), kThreads, 0, s, d_cell_start,
+           d_sorted_ids, n_col, n_row, nbc, slots, cnt.get(), d_order);
 }
 
 void interleave_xy(const double* d_x, const double* d_y, size_t n, double2* d_xy,

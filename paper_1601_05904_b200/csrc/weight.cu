@@ -45,7 +45,7 @@ namespace {
 constexpr int kK4Threads = 256;
 constexpr int kStages = 4;
 constexpr int kMaxChunks = 16;
-constexpr int kTileFloats = 6 * kWeightTile;  // SoA tile: xh yh xl yl zh zl
+constexpr int kTileFloats = 9 * kWeightTile;  // SoA tile, 9 components (see kComps)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -107,44 +107,56 @@ __device__ __forceinline__ void split_hilo(double v, float& hi, float& lo) {
     lo = __double2float_rn(v - static_cast<double>(hi));
 }
 
-// Record i = data point order[i] (cell order of the factor-4 grid, so a
-// 256-point tile is a compact strip of cells), or point i without order.
+// SoA components of a 256-record data tile:
+//   near form  x_hi y_hi x_lo y_lo z_hi z_lo   (unit-box coordinates, hi/lo)
+//   far form   px2 = -2 p'x, py2 = -2 p'y, pp = |p'|^2 with p' = p - c, c the
+//              tile's centre — d2 = |q'|^2 + px2 q'x + py2 q'y + pp in 3 FP32
+//              ops per pair; z_hi is shared with the near form
+enum : int { kXH, kYH, kXL, kYL, kZH, kZL, kPX, kPY, kPP, kComps };
+static_assert(kComps * kWeightTile == kTileFloats, "tile layout");
+
+// Record i = data point order[i] (8 x 8-cell blocks of the factor-4 grid, so
+// a 256-point tile is a compact square), or point i without order.
 __global__ void prep_data_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                  const double* __restrict__ z, const uint32_t* __restrict__ order,
                                  size_t m, size_t mp, double ox, double oy, double inv_scale,
                                  double zmul, float* __restrict__ rec) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= mp) return;
+    float* r = rec + (i / kWeightTile) * kTileFloats + (i % kWeightTile);
     if (i < m) {
         const size_t j = order ? order[i] : i;
-        float xh, xl, yh, yl;
+        float xh, xl, yh, yl, zh, zl;
         split_hilo((x[j] - ox) * inv_scale, xh, xl);
         split_hilo((y[j] - oy) * inv_scale, yh, yl);
-        float* r = rec + (i / kWeightTile) * kTileFloats + (i % kWeightTile);
-        float zh, zl;
         split_hilo(z[j] * zmul, zh, zl);
-        r[0] = xh, r[kWeightTile] = yh, r[2 * kWeightTile] = xl, r[3 * kWeightTile] = yl;
-        r[4 * kWeightTile] = zh, r[5 * kWeightTile] = zl;
-    } else {
-        float* r = rec + (i / kWeightTile) * kTileFloats + (i % kWeightTile);
-        r[0] = 1.0e30f, r[kWeightTile] = 1.0e30f, r[2 * kWeightTile] = 0.0f;
-        r[3 * kWeightTile] = 0.0f, r[4 * kWeightTile] = 0.0f, r[5 * kWeightTile] = 0.0f;
+        r[kXH * kWeightTile] = xh, r[kYH * kWeightTile] = yh;
+        r[kXL * kWeightTile] = xl, r[kYL * kWeightTile] = yl;
+        r[kZH * kWeightTile] = zh, r[kZL * kWeightTile] = zl;
+    } else {  // padding: weight exactly 0 in the near form (the only one a
+              // partial tile uses)
+        r[kXH * kWeightTile] = 1.0e30f, r[kYH * kWeightTile] = 1.0e30f;
+        r[kXL * kWeightTile] = 0.0f, r[kYL * kWeightTile] = 0.0f;
+        r[kZH * kWeightTile] = 0.0f, r[kZL * kWeightTile] = 0.0f;
     }
 }
 
-// Bounding box (hi parts) of each 256-point tile's real records; one warp
-// per tile.  Drives the per-(query, tile) near / far choice in K4.
-__global__ void tile_box_kernel(const float* __restrict__ rec, size_t m, size_t tiles,
-                                float4* __restrict__ box) {
+// One warp per tile: bounding box of the real records (hi parts), centre c,
+// near threshold, and the far-form components.  A (query, tile) pair is FAR
+// when the query's distance to the box exceeds both R_far and the box
+// diagonal: then |q'| + |p'| <= 2 d, so the expanded d2 loses at most a few
+// ulp of d2 (~1e-7 relative), against ~1e-6 for plain hi differences.
+// Partial (padded) tiles are always NEAR.
+__global__ void tile_geo_kernel(float* __restrict__ rec, size_t m, size_t tiles, float rfar2,
+                                float4* __restrict__ box, float4* __restrict__ geo) {
     const size_t tile = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (tile >= tiles) return;
+    float* t = rec + tile * kTileFloats;
     float x0 = 3.0e38f, y0 = 3.0e38f, x1 = -3.0e38f, y1 = -3.0e38f;
     for (int j = lane; j < kWeightTile; j += 32) {
-        const size_t i = tile * kWeightTile + j;
-        if (i < m) {
-            const float px = rec[tile * kTileFloats + j];
-            const float py = rec[tile * kTileFloats + kWeightTile + j];
+        if (tile * kWeightTile + j < m) {
+            const float px = t[kXH * kWeightTile + j], py = t[kYH * kWeightTile + j];
             x0 = fminf(x0, px), y0 = fminf(y0, py), x1 = fmaxf(x1, px), y1 = fmaxf(y1, py);
         }
     }
@@ -155,38 +167,102 @@ __global__ void tile_box_kernel(const float* __restrict__ rec, size_t m, size_t 
         x1 = fmaxf(x1, __shfl_xor_sync(0xFFFFFFFFu, x1, o));
         y1 = fmaxf(y1, __shfl_xor_sync(0xFFFFFFFFu, y1, o));
     }
-    if (lane == 0) box[tile] = make_float4(x0, y0, x1, y1);
+    const float cx = 0.5f * (x0 + x1), cy = 0.5f * (y0 + y1);
+    const float gx = x1 - x0, gy = y1 - y0;
+    const bool partial = (tile + 1) * kWeightTile > m;
+    const float thr2 = partial ? INFINITY : fmaxf(rfar2, 1.001f * fmaf(gx, gx, gy * gy));
+    if (lane == 0) {
+        box[tile] = make_float4(x0, y0, x1, y1);
+        geo[tile] = make_float4(cx, cy, thr2, 0.0f);
+    }
+    for (int j = lane; j < kWeightTile; j += 32) {
+        float px2 = 0.0f, py2 = 0.0f, pp = 0.0f;
+        if (tile * kWeightTile + j < m) {
+            const double px = (static_cast<double>(t[kXH * kWeightTile + j]) - cx) +
+                              static_cast<double>(t[kXL * kWeightTile + j]);
+            const double py = (static_cast<double>(t[kYH * kWeightTile + j]) - cy) +
+                              static_cast<double>(t[kYL * kWeightTile + j]);
+            px2 = __double2float_rn(-2.0 * px);
+            py2 = __double2float_rn(-2.0 * py);
+            pp = __double2float_rn(px * px + py * py);
+        }
+        t[kPX * kWeightTile + j] = px2;
+        t[kPY * kWeightTile + j] = py2;
+        t[kPP * kWeightTile + j] = pp;
+    }
 }
 
 std::atomic<bool> g_alpha4_recipe{true};
 
+// Recipe-class range: alpha == 4 queries take w' = 1 / (d2 s)^2 with s a
+// power of two (exact) putting d2min s in [1e-9, 2e-9) when d2min < 1e-9,
+// else s = 1; the far path pairs two points per reciprocal, so (d2 s)^4
+// products must stay inside FP32: d2min >= kRecipeMinD2 (unit-box units).
+// Smaller non-snapped d2min (< 1e-8.5 of the domain) take the general path.
+constexpr double kRecipeMinD2 = 1.0e-17;
+constexpr double kRecipeLowD2 = 1.0e-9;
+
 // Query classes: A = the exact alpha == 4 recipe (or snapped: result
 // replaced anyway); the other (general-alpha) queries split into G1 (exp2 on
 // MUFU) and G2 (exp2 as a polynomial on the FMA pipe) by a hash of the
-// query's own coordinates — a function of the query alone, so its formula
-// (and result) never depends on sharding, order or GPU count.  Half / half
+// query's normalised FP32 coordinates (the hi parts K4 itself uses) — a
+// function of the query alone, so its formula (and result) never depends on
+// sharding, order or GPU count, and frame-relative, so translating the whole
+// problem (acceptance criterion 5, 1e-9) does not re-class it.  Half / half
 // balances the MUFU and FMA pipes.
-__device__ __forceinline__ bool poly_class(double x, double y) {
-    unsigned long long h = static_cast<unsigned long long>(__double_as_longlong(x)) *
-                           0x9E3779B97F4A7C15ull;
-    h ^= static_cast<unsigned long long>(__double_as_longlong(y)) * 0xC2B2AE3D27D4EB4Full;
-    h ^= h >> 29;
-    return (h >> 63) != 0;
+__device__ __forceinline__ bool poly_class(float xh, float yh) {
+    unsigned h = static_cast<unsigned>(__float_as_int(xh)) * 0x9E3779B1u;
+    h ^= static_cast<unsigned>(__float_as_int(yh)) * 0x85EBCA77u;
+    h ^= h >> 15;
+    h *= 0xC2B2AE3Du;
+    return (h >> 31) != 0;
 }
 
-__global__ void class_flags_kernel(const WeightQueries q, int recipe,
-                                   uint32_t* __restrict__ flag_a, uint32_t* __restrict__ flag_g2) {
+// K4 visiting order: positions sorted along a Morton (Z) curve of the
+// normalised query coordinates, so the 128 queries of a warp and the 1024 of
+// a CTA are spatially compact — they agree on which tiles are near, which
+// keeps the warps of a CTA in step.  (The order never changes a result.)
+__device__ __forceinline__ uint32_t spread16(uint32_t v) {
+    v &= 0xFFFFu;
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+
+__global__ void morton_keys_kernel(const WeightQueries q, WeightFrame f, uint32_t* __restrict__ key,
+                                   uint32_t* __restrict__ pos) {
     const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p >= q.n) return;
-    const bool a = (recipe && q.alpha_s[p] == 4.0) || q.snap_s[p] != kNoId;
     const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
-    flag_a[p] = a ? 1u : 0u;
-    flag_g2[p] = (!a && poly_class(q.qx[qi], q.qy[qi])) ? 1u : 0u;
+    const double xn = (q.qx[qi] - f.ox) * f.inv_scale, yn = (q.qy[qi] - f.oy) * f.inv_scale;
+    const uint32_t cx = static_cast<uint32_t>(fmin(fmax(xn * 65536.0, 0.0), 65535.0));
+    const uint32_t cy = static_cast<uint32_t>(fmin(fmax(yn * 65536.0, 0.0), 65535.0));
+    key[p] = spread16(cx) | (spread16(cy) << 1);
+    pos[p] = static_cast<uint32_t>(p);
+}
+
+// Flags by Morton rank j (p = zpos[j]).
+__global__ void class_flags_kernel(const WeightQueries q, WeightFrame f, int recipe,
+                                   const uint32_t* __restrict__ zpos,
+                                   uint32_t* __restrict__ flag_a, uint32_t* __restrict__ flag_g2) {
+    const size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= q.n) return;
+    const size_t p = zpos[j];
+    const double d2n = q.d2min_s[p] * f.inv_scale * f.inv_scale;
+    const bool a = (recipe && q.alpha_s[p] == 4.0 && d2n >= kRecipeMinD2) || q.snap_s[p] != kNoId;
+    const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
+    flag_a[j] = a ? 1u : 0u;
+    const float xh = __double2float_rn((q.qx[qi] - f.ox) * f.inv_scale);
+    const float yh = __double2float_rn((q.qy[qi] - f.oy) * f.inv_scale);
+    flag_g2[j] = (!a && poly_class(xh, yh)) ? 1u : 0u;
 }
 
 // 3-way partition (general G1/G2 interleaved, then A) fused with the
 // per-query record build.
 __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
+                                     const uint32_t* __restrict__ zpos,
                                      const uint32_t* __restrict__ flag_a,
                                      const uint32_t* __restrict__ scan_a,
                                      const uint32_t* __restrict__ flag_g2,
@@ -194,21 +270,22 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
                                      uint32_t* __restrict__ order, float4* __restrict__ qhl,
                                      float4* __restrict__ qpar, double* __restrict__ lshift,
                                      unsigned long long* __restrict__ alpha4) {
-    const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (p >= q.n) return;
+    const size_t jz = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (jz >= q.n) return;
+    const size_t p = zpos[jz];
     const size_t num_a = static_cast<size_t>(scan_a[q.n - 1]) + flag_a[q.n - 1];
     const size_t num_g2 = static_cast<size_t>(scan_g2[q.n - 1]) + flag_g2[q.n - 1];
     const size_t num_g1 = q.n - num_a - num_g2;
-    const bool is_a = flag_a[p] != 0, is_g2 = flag_g2[p] != 0;
+    const bool is_a = flag_a[jz] != 0, is_g2 = flag_g2[jz] != 0;
     // General queries: 64-query blocks of G1 and G2 alternate, so a warp's
     // pair 0 (slots 0, 1) is G1 and pair 1 (slots 2, 3) is G2 — each warp
     // issues MUFU and FMA-pipe exponentials side by side.  Leftovers follow.
     // The general region comes first so its 128-query blocks align with warps.
     size_t i;
     if (is_a) {
-        i = num_g1 + num_g2 + scan_a[p];
+        i = num_g1 + num_g2 + scan_a[jz];
     } else {
-        const size_t j = is_g2 ? scan_g2[p] : p - scan_a[p] - scan_g2[p];
+        const size_t j = is_g2 ? scan_g2[jz] : jz - scan_a[jz] - scan_g2[jz];
         const size_t both = (num_g1 < num_g2 ? num_g1 : num_g2) / 64;  // full block pairs
         if (j < 64 * both) {
             i = (j / 64) * 128 + (is_g2 ? 64 : 0) + (j % 64);
@@ -229,15 +306,13 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
     const float c = __double2float_rn(-0.5 * alpha);
     // general path: w' = ex2(c lg2(d2) + b) with b = -c lg2(d2min) so w' <= 1
     const float b = __double2float_rn(-static_cast<double>(c) * log2(d2n));
-    // recipe path: w' = rcp((d2 s)^2).  s = 1 (no multiply needed, exact)
-    // whenever d2 >= d2min >= 1e-15 keeps d2^2 and 1/d2^2 inside FP32;
-    // otherwise s = 1/d2min.  Snapped queries: result replaced, s = 1.
+    // recipe path: w' = rcp((d2 s)^2), s = 1 or a power of two (exact)
     const bool snapped = q.snap_s[p] != kNoId;
-    const float s = (snapped || d2n >= 1.0e-15) ? 1.0f : __double2float_rn(1.0 / d2n);
-    qpar[i] = make_float4(c, b, s, is_a ? 1.0f : (is_g2 ? 2.0f : 0.0f));
+    const double s = (snapped || d2n >= kRecipeLowD2) ? 1.0 : exp2(ceil(log2(kRecipeLowD2 / d2n)));
+    qpar[i] = make_float4(c, b, static_cast<float>(s), is_a ? 1.0f : (is_g2 ? 2.0f : 0.0f));
     // log2(true weight) = log2(kernel weight) + shift (settle's overflow test)
     const double l2inv = log2(f.inv_scale);
-    lshift[i] = is_a ? 2.0 * log2(static_cast<double>(s)) + 4.0 * l2inv
+    lshift[i] = is_a ? 2.0 * log2(s) + 4.0 * l2inv
                      : -static_cast<double>(b) - 2.0 * static_cast<double>(c) * l2inv;
     if (alpha == 4.0 && alpha4) atomicAdd(alpha4, 1ull);
 }
@@ -250,9 +325,11 @@ struct K4Args {
     const float4* qhl;
     const float4* qpar;
     size_t n;
-    double2* part;  // n * chunks
-    const float4* tile_box;  // hi-coordinate box of every tile's real records
-    float rfar2;             // squared near / far threshold (unit-box units)
+    const uint32_t* flag_a;  // class counts: A = scan_a[n-1] + flag_a[n-1]
+    const uint32_t* scan_a;
+    double2* part;            // n * chunks, by visiting position
+    const float4* tile_box;   // hi-coordinate box of every tile's real records
+    const float4* tile_geo;   // {cx, cy, near threshold^2, 0}
 };
 
 // ---- packed f32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2): two queries per
@@ -264,6 +341,7 @@ __device__ __forceinline__ f2 pk2(float lo, float hi) {
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
     return r;
 }
+__device__ __forceinline__ f2 bc2(float v) { return pk2(v, v); }
 __device__ __forceinline__ void up2(f2 v, float& lo, float& hi) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
@@ -286,6 +364,11 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
     f2 r;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
+}
+__device__ __forceinline__ f2 rcp2(f2 v) {
+    float lo, hi;
+    up2(v, lo, hi);
+    return pk2(mufu_rcp(lo), mufu_rcp(hi));
 }
 
 // exp2 on the FMA pipe for class-G2 queries (x <= ~0 after ratio scaling):
@@ -316,15 +399,15 @@ __device__ __forceinline__ f2 exp2_fma2(f2 x) {
     float lo, hi;
     up2(x, lo, hi);
     const f2 xc = pk2(fmaxf(lo, -125.0f), fmaxf(hi, -125.0f));
-    const f2 m = pk2(kExpMagic, kExpMagic);
+    const f2 m = bc2(kExpMagic);
     const f2 t = add2(xc, m);
     const f2 f = sub2(xc, sub2(t, m));
-    f2 p = fma2(pk2(kE6, kE6), f, pk2(kE5, kE5));
-    p = fma2(p, f, pk2(kE4, kE4));
-    p = fma2(p, f, pk2(kE3, kE3));
-    p = fma2(p, f, pk2(kE2, kE2));
-    p = fma2(p, f, pk2(kE1, kE1));
-    p = fma2(p, f, pk2(kE0, kE0));
+    f2 p = fma2(bc2(kE6), f, bc2(kE5));
+    p = fma2(p, f, bc2(kE4));
+    p = fma2(p, f, bc2(kE3));
+    p = fma2(p, f, bc2(kE2));
+    p = fma2(p, f, bc2(kE1));
+    p = fma2(p, f, bc2(kE0));
     float plo, phi, tlo, thi;
     up2(p, plo, phi);
     up2(t, tlo, thi);
@@ -333,251 +416,296 @@ __device__ __forceinline__ f2 exp2_fma2(f2 x) {
 }
 
 // Per-thread query state: QT queries as QT/2 f32x2 pairs.
+// The coordinates are re-read per tile (L1-resident, 4 x 16 B per thread per
+// 256-point tile) instead of being held across the tile loop: the far pass
+// needs only the tile-relative q', and registers bound occupancy.
 template <int QT>
 struct QState {
     static constexpr int kPairs = QT / 2;
-    f2 xh[kPairs], yh[kPairs], xl[kPairs], yl[kPairs];
     f2 c[kPairs], b[kPairs], s[kPairs];
-    bool a[QT];   // class A (alpha == 4 recipe), per query
     bool g2[QT];  // class G2 (FMA-pipe exp2), per query
-    bool v[QT];  // query slot holds a real query
+    bool v[QT];   // query slot holds a real query
 };
 
-// One 256-point tile against the thread's QT queries.  Per data point and
-// query pair:
-//   NEAR tile (the query lies within R_far of the tile's box): hi/lo
-//     differences, dx = (x_hi - q_hi) + (x_lo - q_lo): 3 FADD2 each for dx, dy
-//   FAR tile: dx = x_hi - q_hi: 1 FADD2 each (relative error <= 6e-8 / R_far
-//     on pairs that carry a small share of the weight)
-//   d2 = dx dx + dy dy: FMUL2 + FFMA2, then
-//   MODE 3 (alpha == 4 recipe, s == 1): FMUL2 (d2^2), 2 x MUFU.RCP
-//   MODE 0 (alpha == 4 recipe, scaled): FMUL2 (d2 s), FMUL2 (^2), 2 x MUFU.RCP
-//   MODE 1 (general, G1):       2 x MUFU.LG2, FFMA2 (c lg + b), 2 x MUFU.EX2
-//   MODE 4 (general, G2):       2 x MUFU.LG2, FFMA2, exp2 on the FMA pipe
-//   MODE 5 (G1 pair 0, G2 pair 1): both of the above in one instruction stream
-//   MODE 2 (mixed class warp):  per query class and near flag, scalar, same roundings
-// and FADD2 (sum w) + FFMA2 (sum w z) — Kahan-compensated with hi/lo z in
-// NEAR tiles, where a query's large terms live.  DIST: 0 = every query of
-// the warp far, 1 = every query near, 2 = mixed (both forms, per-lane
-// select).  The formula is a function of the (query, tile) pair only, so a
-// query's result never depends on its warp or lane.
-__device__ __forceinline__ f2 sel2(f2 a, f2 b, bool take_a_lo, bool take_a_hi) {
-    float alo, ahi, blo, bhi;
-    up2(a, alo, ahi);
-    up2(b, blo, bhi);
-    return pk2(take_a_lo ? alo : blo, take_a_hi ? ahi : bhi);
+// Query coordinates {x_hi, y_hi, x_lo, y_lo} of a pair of slots (volatile:
+// each pass re-reads instead of keeping them live).
+struct QCoords {
+    f2 xh, yh, xl, yl;
+};
+__device__ __forceinline__ float4 ld_q(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+template <int QT>
+__device__ __forceinline__ void load_coords(const float4* qhl, size_t wbase, int lane, size_t q1,
+                                            QCoords (&qc)[QT / 2]) {
+#pragma unroll
+    for (int k = 0; k < QT / 2; ++k) {
+        const size_t p0 = wbase + static_cast<size_t>(2 * k) * 32 + lane;
+        const size_t p1 = p0 + 32;
+        const float4 h0 = p0 < q1 ? ld_q(qhl + p0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 h1 = p1 < q1 ? ld_q(qhl + p1) : make_float4(0.f, 0.f, 0.f, 0.f);
+        qc[k].xh = pk2(h0.x, h1.x);
+        qc[k].yh = pk2(h0.y, h1.y);
+        qc[k].xl = pk2(h0.z, h1.z);
+        qc[k].yl = pk2(h0.w, h1.w);
+    }
 }
 
-// One data point (scalars from the SoA tile) against the thread's queries.
-template <int MODE, int DIST, int QT>
-__device__ __forceinline__ void k4_point(float pxh, float pyh, float pxl, float pyl, float pzh,
-                                         float pzl, const QState<QT>& q, const bool (&nq)[QT],
-                                         f2 (&sw)[QT / 2], f2 (&swz)[QT / 2],
-                                         f2 (&cz)[QT / 2]) {
+// Weight formula modes (warp-uniform; per query the arithmetic is the same
+// in every mode that can hold it, so grouping never changes a result):
+//   3  recipe, s == 1 for the whole warp      w' = rcp(d2^2)
+//   0  recipe, some s != 1                    w' = rcp((d2 s)^2)
+//   1  general, all G1                        w' = ex2(c lg2(d2) + b)  (2 MUFU)
+//   4  general, all G2                        ex2 on the FMA pipe      (1 MUFU)
+//   5  general, pair 0 G1 / pair 1 G2 (the interleaved layout)
+//   2  general, G1 and G2 mixed otherwise (per query, scalar)
+template <int MODE, int QT>
+__device__ __forceinline__ f2 general_w(f2 d2, const QState<QT>& q, int r) {
+    float lo, hi;
+    up2(d2, lo, hi);
+    if (MODE == 2) {
+        const bool g0 = q.g2[2 * r], g1 = q.g2[2 * r + 1];
+        float c0, c1, b0, b1;
+        up2(q.c[r], c0, c1);
+        up2(q.b[r], b0, b1);
+        const float e0 = fmaf(c0, mufu_lg2(lo), b0), e1 = fmaf(c1, mufu_lg2(hi), b1);
+        return pk2(g0 ? exp2_fma(e0) : mufu_ex2(e0), g1 ? exp2_fma(e1) : mufu_ex2(e1));
+    }
+    const f2 e = fma2(q.c[r], pk2(mufu_lg2(lo), mufu_lg2(hi)), q.b[r]);
+    if (MODE == 4 || (MODE == 5 && r % 2 == 1)) return exp2_fma2(e);
+    up2(e, lo, hi);
+    return pk2(mufu_ex2(lo), mufu_ex2(hi));
+}
+
+// FAR tile: d2 = fma(py2, q'y, fma(px2, q'x, |q'|^2)) + pp, 3 FP32 ops per
+// pair; sums plain (far pairs carry a small weight share or average out).
+// Recipe modes pair points 4j and 4j+1 on one reciprocal,
+//   w0 + w1 = (a0 + a1) rcp(a0 a1),  w0 z0 + w1 z1 = (a1 z0 + a0 z1) rcp(a0 a1),
+// a = (d2 s)^2 — 6.5 FP32 ops + 0.75 MUFU per pair, balancing the FMA pipe
+// (128 lanes / clk / SM) against MUFU (16 / clk / SM).
+template <int MODE, int QT>
+__device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState<QT>& q,
+                                       const f2 (&fx)[QT / 2], const f2 (&fy)[QT / 2],
+                                       const f2 (&fq)[QT / 2], f2 (&sw)[QT / 2],
+                                       f2 (&swz)[QT / 2]) {
     constexpr int kPairs = QT / 2;
-    const f2 px = pk2(pxh, pxh), py = pk2(pyh, pyh), pz = pk2(pzh, pzh);
+#pragma unroll 2
+    for (int j = 0; j < kWeightTile; j += 4) {
+        const float4 X = *reinterpret_cast<const float4*>(t + kPX * kWeightTile + j);
+        const float4 Y = *reinterpret_cast<const float4*>(t + kPY * kWeightTile + j);
+        const float4 P = *reinterpret_cast<const float4*>(t + kPP * kWeightTile + j);
+        const float4 Z = *reinterpret_cast<const float4*>(t + kZH * kWeightTile + j);
 #pragma unroll
-    for (int r = 0; r < kPairs; ++r) {
-        f2 w;
-        if (MODE == 2) {
-            float xh[2], yh[2], xl[2], yl[2], cc[2], bb[2], ss[2], ww[2];
-            up2(q.xh[r], xh[0], xh[1]);
-            up2(q.yh[r], yh[0], yh[1]);
-            up2(q.xl[r], xl[0], xl[1]);
-            up2(q.yl[r], yl[0], yl[1]);
-            up2(q.c[r], cc[0], cc[1]);
-            up2(q.b[r], bb[0], bb[1]);
-            up2(q.s[r], ss[0], ss[1]);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float dx = pxh - xh[h], dy = pyh - yh[h];
-                if (nq[2 * r + h]) {
-                    dx = dx + (pxl - xl[h]);
-                    dy = dy + (pyl - yl[h]);
+        for (int r = 0; r < kPairs; ++r) {
+            f2 d0 = add2(fma2(bc2(Y.x), fy[r], fma2(bc2(X.x), fx[r], fq[r])), bc2(P.x));
+            f2 d1 = add2(fma2(bc2(Y.y), fy[r], fma2(bc2(X.y), fx[r], fq[r])), bc2(P.y));
+            f2 d2 = add2(fma2(bc2(Y.z), fy[r], fma2(bc2(X.z), fx[r], fq[r])), bc2(P.z));
+            f2 d3 = add2(fma2(bc2(Y.w), fy[r], fma2(bc2(X.w), fx[r], fq[r])), bc2(P.w));
+            if (MODE == 3 || MODE == 0) {
+                if (MODE == 0) {
+                    d0 = mul2(d0, q.s[r]);
+                    d1 = mul2(d1, q.s[r]);
+                    d2 = mul2(d2, q.s[r]);
+                    d3 = mul2(d3, q.s[r]);
                 }
-                const float d2 = fmaf(dx, dx, dy * dy);
-                if (q.a[2 * r + h]) {
-                    const float t = d2 * ss[h];
-                    ww[h] = mufu_rcp(t * t);
-                } else {
-                    const float e = fmaf(cc[h], mufu_lg2(d2), bb[h]);
-                    ww[h] = q.g2[2 * r + h] ? exp2_fma(e) : mufu_ex2(e);
-                }
-            }
-            w = pk2(ww[0], ww[1]);
-        } else {
-            f2 dx = sub2(px, q.xh[r]), dy = sub2(py, q.yh[r]);
-            if (DIST == 1) {
-                dx = add2(dx, sub2(pk2(pxl, pxl), q.xl[r]));
-                dy = add2(dy, sub2(pk2(pyl, pyl), q.yl[r]));
-            } else if (DIST == 2) {
-                dx = sel2(add2(dx, sub2(pk2(pxl, pxl), q.xl[r])), dx, nq[2 * r], nq[2 * r + 1]);
-                dy = sel2(add2(dy, sub2(pk2(pyl, pyl), q.yl[r])), dy, nq[2 * r], nq[2 * r + 1]);
-            }
-            const f2 d2 = fma2(dx, dx, mul2(dy, dy));
-            float lo, hi;
-            if (MODE == 3) {  // recipe, s == 1 for every query of the warp
-                up2(mul2(d2, d2), lo, hi);
-                w = pk2(mufu_rcp(lo), mufu_rcp(hi));
-            } else if (MODE == 0) {
-                const f2 t = mul2(d2, q.s[r]);
-                up2(mul2(t, t), lo, hi);
-                w = pk2(mufu_rcp(lo), mufu_rcp(hi));
-            } else if (MODE == 4 || (MODE == 5 && r % 2 == 1)) {  // G2: FMA-pipe exp2
-                up2(d2, lo, hi);
-                w = exp2_fma2(fma2(q.c[r], pk2(mufu_lg2(lo), mufu_lg2(hi)), q.b[r]));
+                const f2 a0 = mul2(d0, d0), a1 = mul2(d1, d1);
+                const f2 a2 = mul2(d2, d2), a3 = mul2(d3, d3);
+                const f2 r01 = rcp2(mul2(a0, a1));
+                sw[r] = fma2(r01, add2(a0, a1), sw[r]);
+                swz[r] = fma2(r01, fma2(a1, bc2(Z.x), mul2(a0, bc2(Z.y))), swz[r]);
+                const f2 w2 = rcp2(a2);
+                sw[r] = add2(sw[r], w2);
+                swz[r] = fma2(w2, bc2(Z.z), swz[r]);
+                const f2 w3 = rcp2(a3);
+                sw[r] = add2(sw[r], w3);
+                swz[r] = fma2(w3, bc2(Z.w), swz[r]);
             } else {
-                up2(d2, lo, hi);
-                up2(fma2(q.c[r], pk2(mufu_lg2(lo), mufu_lg2(hi)), q.b[r]), lo, hi);
-                w = pk2(mufu_ex2(lo), mufu_ex2(hi));
-            }
-        }
-        sw[r] = add2(sw[r], w);
-        if (MODE == 2) {  // per query: compensated when near, plain when far
-            float wv[2], sv[2], cv[2];
-            up2(w, wv[0], wv[1]);
-            up2(swz[r], sv[0], sv[1]);
-            up2(cz[r], cv[0], cv[1]);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (nq[2 * r + h]) {
-                    const float t = fmaf(wv[h], pzh, wv[h] * pzl);
-                    const float y = t - cv[h];
-                    const float s2 = sv[h] + y;
-                    cv[h] = (s2 - sv[h]) - y;
-                    sv[h] = s2;
-                } else {
-                    sv[h] = fmaf(wv[h], pzh, sv[h]);
-                }
-            }
-            swz[r] = pk2(sv[0], sv[1]);
-            cz[r] = pk2(cv[0], cv[1]);
-        } else if (DIST == 0) {
-            swz[r] = fma2(w, pz, swz[r]);
-        } else {  // Kahan-compensated w z with hi/lo z
-            const f2 t = fma2(w, pz, mul2(w, pk2(pzl, pzl)));
-            const f2 y = sub2(t, cz[r]);
-            const f2 s2 = add2(swz[r], y);
-            const f2 c2 = sub2(sub2(s2, swz[r]), y);
-            if (DIST == 1) {
-                cz[r] = c2;
-                swz[r] = s2;
-            } else {
-                cz[r] = sel2(c2, cz[r], nq[2 * r], nq[2 * r + 1]);
-                swz[r] = sel2(s2, fma2(w, pz, swz[r]), nq[2 * r], nq[2 * r + 1]);
+                const f2 w0 = general_w<MODE, QT>(d0, q, r);
+                sw[r] = add2(sw[r], w0);
+                swz[r] = fma2(w0, bc2(Z.x), swz[r]);
+                const f2 w1 = general_w<MODE, QT>(d1, q, r);
+                sw[r] = add2(sw[r], w1);
+                swz[r] = fma2(w1, bc2(Z.y), swz[r]);
+                const f2 w2 = general_w<MODE, QT>(d2, q, r);
+                sw[r] = add2(sw[r], w2);
+                swz[r] = fma2(w2, bc2(Z.z), swz[r]);
+                const f2 w3 = general_w<MODE, QT>(d3, q, r);
+                sw[r] = add2(sw[r], w3);
+                swz[r] = fma2(w3, bc2(Z.w), swz[r]);
             }
         }
     }
 }
 
-// One 256-point tile, stored SoA in shared memory as
-//   [x_hi | y_hi | x_lo | y_lo | z_hi | z_lo] x 256 floats,
-// so one LDS.128 fetches a component of 4 consecutive points (far tiles read
-// 3 components, near tiles 6: 0.75-1.5 LDS per 4 points per thread instead
-// of 8), which keeps the MIO queue free for the MUFU work.
-template <int MODE, int DIST, int QT>
-__device__ __forceinline__ void k4_tile(const float* __restrict__ t, const QState<QT>& q,
-                                        const bool (&nq)[QT], f2 (&sw)[QT / 2],
+// NEAR tile (the query lies within the near threshold of the tile's box, or
+// the tile is padded): hi/lo differences dx = (x_hi - q_hi) + (x_lo - q_lo)
+// (~48 bits), one reciprocal / exponential per pair, and sum w z
+// Kahan-compensated with hi/lo z — a query's dominant terms live here.
+template <int MODE, int QT>
+__device__ __forceinline__ void k4_near_point(float pxh, float pyh, float pxl, float pyl,
+                                              float pzh, float pzl, const QState<QT>& q,
+                                              const QCoords (&qc)[QT / 2], f2 (&sw)[QT / 2],
+                                              f2 (&swz)[QT / 2], f2 (&cz)[QT / 2]) {
+    constexpr int kPairs = QT / 2;
+#pragma unroll
+    for (int r = 0; r < kPairs; ++r) {
+        const f2 dx = add2(sub2(bc2(pxh), qc[r].xh), sub2(bc2(pxl), qc[r].xl));
+        const f2 dy = add2(sub2(bc2(pyh), qc[r].yh), sub2(bc2(pyl), qc[r].yl));
+        f2 d2 = fma2(dx, dx, mul2(dy, dy));
+        f2 w;
+        if (MODE == 3 || MODE == 0) {
+            if (MODE == 0) d2 = mul2(d2, q.s[r]);
+            w = rcp2(mul2(d2, d2));
+        } else {
+            w = general_w<MODE, QT>(d2, q, r);
+        }
+        sw[r] = add2(sw[r], w);
+        const f2 tz = fma2(w, bc2(pzh), mul2(w, bc2(pzl)));
+        const f2 y = sub2(tz, cz[r]);
+        const f2 s2 = add2(swz[r], y);
+        cz[r] = sub2(sub2(s2, swz[r]), y);
+        swz[r] = s2;
+    }
+}
+
+template <int MODE, int QT>
+__device__ __forceinline__ void k4_near(const float* __restrict__ t, const QState<QT>& q,
+                                        const QCoords (&qc)[QT / 2], f2 (&sw)[QT / 2],
                                         f2 (&swz)[QT / 2], f2 (&cz)[QT / 2]) {
 #pragma unroll 1
     for (int j = 0; j < kWeightTile; j += 4) {
-        const float4 X = *reinterpret_cast<const float4*>(t + j);
-        const float4 Y = *reinterpret_cast<const float4*>(t + kWeightTile + j);
-        const float4 Z = *reinterpret_cast<const float4*>(t + 4 * kWeightTile + j);
-        float4 XL = make_float4(0.f, 0.f, 0.f, 0.f), YL = XL, ZL = XL;
-        if (DIST != 0 || MODE == 2) {
-            XL = *reinterpret_cast<const float4*>(t + 2 * kWeightTile + j);
-            YL = *reinterpret_cast<const float4*>(t + 3 * kWeightTile + j);
-            ZL = *reinterpret_cast<const float4*>(t + 5 * kWeightTile + j);
-        }
-        k4_point<MODE, DIST, QT>(X.x, Y.x, XL.x, YL.x, Z.x, ZL.x, q, nq, sw, swz, cz);
-        k4_point<MODE, DIST, QT>(X.y, Y.y, XL.y, YL.y, Z.y, ZL.y, q, nq, sw, swz, cz);
-        k4_point<MODE, DIST, QT>(X.z, Y.z, XL.z, YL.z, Z.z, ZL.z, q, nq, sw, swz, cz);
-        k4_point<MODE, DIST, QT>(X.w, Y.w, XL.w, YL.w, Z.w, ZL.w, q, nq, sw, swz, cz);
+        const float4 X = *reinterpret_cast<const float4*>(t + kXH * kWeightTile + j);
+        const float4 Y = *reinterpret_cast<const float4*>(t + kYH * kWeightTile + j);
+        const float4 XL = *reinterpret_cast<const float4*>(t + kXL * kWeightTile + j);
+        const float4 YL = *reinterpret_cast<const float4*>(t + kYL * kWeightTile + j);
+        const float4 Z = *reinterpret_cast<const float4*>(t + kZH * kWeightTile + j);
+        const float4 ZL = *reinterpret_cast<const float4*>(t + kZL * kWeightTile + j);
+        k4_near_point<MODE, QT>(X.x, Y.x, XL.x, YL.x, Z.x, ZL.x, q, qc, sw, swz, cz);
+        k4_near_point<MODE, QT>(X.y, Y.y, XL.y, YL.y, Z.y, ZL.y, q, qc, sw, swz, cz);
+        k4_near_point<MODE, QT>(X.z, Y.z, XL.z, YL.z, Z.z, ZL.z, q, qc, sw, swz, cz);
+        k4_near_point<MODE, QT>(X.w, Y.w, XL.w, YL.w, Z.w, ZL.w, q, qc, sw, swz, cz);
     }
 }
 
-template <int kQT, int kMinBlocks>
-__global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4Args a) {
-    constexpr int kPairs = kQT / 2;
-    extern __shared__ __align__(128) unsigned char smem[];
-    float* stile = reinterpret_cast<float*>(smem);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(stile + kStages * kTileFloats);
+// One tile against the thread's queries: far part (queries FAR from the
+// tile) and near part (queries NEAR), each over the whole tile with its own
+// accumulators, only when some query of the warp needs it; each query folds
+// the part its own (query, tile) classification selects into FP64.
+template <int MODE, int QT>
+__device__ __forceinline__ void k4_tile(const float* __restrict__ t, const QState<QT>& q,
+                                        const float4* qhl, size_t wbase, int lane, size_t q1,
+                                        const bool (&nq)[QT], bool any_far, bool any_near,
+                                        float cx, float cy, double (&SW)[QT], double (&SWZ)[QT]) {
+    constexpr int kPairs = QT / 2;
+    if (any_far) {
+        f2 fx[kPairs], fy[kPairs], fq[kPairs], sw[kPairs], swz[kPairs];
+        {
+            QCoords qc[kPairs];
+            load_coords<QT>(qhl, wbase, lane, q1, qc);
+#pragma unroll
+            for (int r = 0; r < kPairs; ++r) {
+                fx[r] = add2(sub2(qc[r].xh, bc2(cx)), qc[r].xl);
+                fy[r] = add2(sub2(qc[r].yh, bc2(cy)), qc[r].yl);
+                fq[r] = fma2(fx[r], fx[r], mul2(fy[r], fy[r]));
+                sw[r] = swz[r] = 0ull;
+            }
+        }
+        k4_far<MODE, QT>(t, q, fx, fy, fq, sw, swz);
+#pragma unroll
+        for (int r = 0; r < kPairs; ++r) {
+            float w0, w1, z0, z1;
+            up2(sw[r], w0, w1);
+            up2(swz[r], z0, z1);
+            if (!nq[2 * r]) SW[2 * r] += w0, SWZ[2 * r] += z0;
+            if (!nq[2 * r + 1]) SW[2 * r + 1] += w1, SWZ[2 * r + 1] += z1;
+        }
+    }
+    if (any_near) {
+        QCoords qc[kPairs];
+        load_coords<QT>(qhl, wbase, lane, q1, qc);
+        f2 sw[kPairs], swz[kPairs], cz[kPairs];
+#pragma unroll
+        for (int r = 0; r < kPairs; ++r) sw[r] = swz[r] = cz[r] = 0ull;
+        k4_near<MODE, QT>(t, q, qc, sw, swz, cz);
+#pragma unroll
+        for (int r = 0; r < kPairs; ++r) {
+            float w0, w1, z0, z1, c0, c1;
+            up2(sw[r], w0, w1);
+            up2(swz[r], z0, z1);
+            up2(cz[r], c0, c1);
+            if (nq[2 * r])
+                SW[2 * r] += w0, SWZ[2 * r] += static_cast<double>(z0) - static_cast<double>(c0);
+            if (nq[2 * r + 1])
+                SW[2 * r + 1] += w1,
+                    SWZ[2 * r + 1] += static_cast<double>(z1) - static_cast<double>(c1);
+        }
+    }
+}
 
+// The CTA body for one query class.  RECIPE: alpha == 4 queries (modes 3 /
+// 0); else the general queries (modes 1 / 4 / 5 / 2).  Each CTA streams the
+// tiles of one data chunk through a kStages-deep shared-memory ring filled
+// by the bulk-copy engine (cp.async.bulk + mbarrier complete_tx; SASS
+// UBLKCP), one elected thread producing, all warps consuming broadcast
+// LDS.128 reads of one component of 4 consecutive points.
+template <bool RECIPE, int kQT>
+__device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, size_t cta,
+                                        float* stile, uint64_t* bar, unsigned* done) {
+    constexpr int kPairs = kQT / 2;
     const unsigned chunk = blockIdx.y;
     const size_t t0 = static_cast<size_t>(chunk) * a.tiles_per_chunk;
     const size_t t1 = t0 + a.tiles_per_chunk < a.tiles ? t0 + a.tiles_per_chunk : a.tiles;
     const size_t ntl = t1 > t0 ? t1 - t0 : 0;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const size_t wbase = static_cast<size_t>(blockIdx.x) * (kK4Threads * kQT) +
-                         static_cast<size_t>(warp) * (32 * kQT);
+    const size_t wbase = q0 + cta * (kK4Threads * kQT) + static_cast<size_t>(warp) * (32 * kQT);
     QState<kQT> q;
-    bool any_a = false, any_g = false, any_g2 = false, any_scaled = false;
+    bool any_g1 = false, any_g2 = false, any_scaled = false;
     {
-        float4 h[kQT], r[kQT];
+        float4 r[kQT];
 #pragma unroll
         for (int i = 0; i < kQT; ++i) {
             const size_t p = wbase + static_cast<size_t>(i) * 32 + lane;
-            h[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            r[i] = make_float4(-1.f, 0.f, 1.f, 1.f);
-            if (p < a.n) {
-                h[i] = a.qhl[p];
-                r[i] = a.qpar[p];
-                q.a[i] = r[i].w == 1.0f;
-                q.g2[i] = r[i].w == 2.0f;
-                any_g2 |= q.g2[i];
-                q.v[i] = true;
-                any_a |= q.a[i];
-                any_g |= !q.a[i] && !q.g2[i];
-                any_scaled |= r[i].z != 1.0f;
-            } else {
-                q.a[i] = true;
-                q.g2[i] = false;
-                q.v[i] = false;
-            }
+            r[i] = make_float4(-1.f, 0.f, 1.f, RECIPE ? 1.f : 0.f);
+            q.v[i] = p < q1;
+            if (q.v[i]) r[i] = a.qpar[p];
+            q.g2[i] = r[i].w == 2.0f;
+            any_g2 |= q.v[i] && q.g2[i];
+            any_g1 |= q.v[i] && !q.g2[i];
+            any_scaled |= q.v[i] && r[i].z != 1.0f;
         }
 #pragma unroll
         for (int k = 0; k < kPairs; ++k) {
             const int i0 = 2 * k, i1 = 2 * k + 1;
-            q.xh[k] = pk2(h[i0].x, h[i1].x);
-            q.yh[k] = pk2(h[i0].y, h[i1].y);
-            q.xl[k] = pk2(h[i0].z, h[i1].z);
-            q.yl[k] = pk2(h[i0].w, h[i1].w);
             q.c[k] = pk2(r[i0].x, r[i1].x);
             q.b[k] = pk2(r[i0].y, r[i1].y);
             q.s[k] = pk2(r[i0].z, r[i1].z);
         }
     }
-    any_a = __any_sync(0xFFFFFFFFu, any_a);
-    any_g = __any_sync(0xFFFFFFFFu, any_g);
+    any_g1 = __any_sync(0xFFFFFFFFu, any_g1);
     any_g2 = __any_sync(0xFFFFFFFFu, any_g2);
     any_scaled = __any_sync(0xFFFFFFFFu, any_scaled);
-    // warp-uniform formula group; per query the arithmetic is identical in
-    // every mode (s == 1 makes d2 * s == d2 exactly), so grouping never
-    // changes a result
-    const int classes = (any_a ? 1 : 0) + (any_g ? 1 : 0) + (any_g2 ? 1 : 0);
-    // the interleaved layout: pair 0 all G1 and pair 1 all G2 across the warp
-    bool split = kQT == 4;
+    int mode;
+    if (RECIPE) {
+        mode = any_scaled ? 0 : 3;
+    } else {
+        // the interleaved layout: pair 0 all G1 and pair 1 all G2 across the warp
+        bool split = kQT == 4;
 #pragma unroll
-    for (int i = 0; i < kQT; ++i) {
-        const bool want_g2 = i >= kQT / 2;
-        split &= !q.v[i] || (!q.a[i] && q.g2[i] == want_g2);
+        for (int i = 0; i < kQT; ++i) split &= !q.v[i] || (q.g2[i] == (i >= kQT / 2));
+        split = __all_sync(0xFFFFFFFFu, split) && any_g1 && any_g2;
+        mode = split ? 5 : (any_g1 && any_g2) ? 2 : any_g2 ? 4 : 1;
     }
-    split = __all_sync(0xFFFFFFFFu, split) && any_g && any_g2;
-    const int mode = split ? 5
-                     : classes > 1 ? 2 : any_g2 ? 4 : any_g ? 1 : (any_scaled ? 0 : 3);
 
     double SW[kQT], SWZ[kQT];
 #pragma unroll
     for (int i = 0; i < kQT; ++i) SW[i] = SWZ[i] = 0.0;
 
     constexpr uint32_t kTileBytes = kTileFloats * sizeof(float);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
     if (threadIdx.x == 0) {
         for (size_t s = 0; s < ntl && s < static_cast<size_t>(kStages); ++s) {
             mbar_expect_tx(&bar[s], kTileBytes);
@@ -588,79 +716,86 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
         const int st = static_cast<int>(it % kStages);
         mbar_wait(&bar[st], static_cast<uint32_t>((it / kStages) & 1));
         const float* tt = stile + st * kTileFloats;
-        f2 sw[kPairs], swz[kPairs], cz[kPairs];
-#pragma unroll
-        for (int k = 0; k < kPairs; ++k) sw[k] = swz[k] = cz[k] = 0ull;
         // per-(query, tile) near flags, then a warp-uniform dispatch
         const float4 tb = __ldg(a.tile_box + t0 + it);
+        const float4 tg = __ldg(a.tile_geo + t0 + it);
         bool nq[kQT];
-        bool any_near = false, all_near = true;
+        bool any_near = false, any_far = false;
 #pragma unroll
-        for (int k = 0; k < kPairs; ++k) {
-            float x[2], y[2];
-            up2(q.xh[k], x[0], x[1]);
-            up2(q.yh[k], y[0], y[1]);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const float ex = fmaxf(0.0f, fmaxf(tb.x - x[h], x[h] - tb.z));
-                const float ey = fmaxf(0.0f, fmaxf(tb.y - y[h], y[h] - tb.w));
-                nq[2 * k + h] = fmaf(ex, ex, ey * ey) <= a.rfar2;
-                if (q.v[2 * k + h]) {  // empty slots never force a mixed tile
-                    any_near |= nq[2 * k + h];
-                    all_near &= nq[2 * k + h];
-                }
+        for (int i = 0; i < kQT; ++i) {
+            const size_t p = wbase + static_cast<size_t>(i) * 32 + lane;
+            const float2 xy = q.v[i] ? __ldg(reinterpret_cast<const float2*>(a.qhl + p))
+                                     : make_float2(0.f, 0.f);
+            const float ex = fmaxf(0.0f, fmaxf(tb.x - xy.x, xy.x - tb.z));
+            const float ey = fmaxf(0.0f, fmaxf(tb.y - xy.y, xy.y - tb.w));
+            nq[i] = fmaf(ex, ex, ey * ey) <= tg.z;
+            if (q.v[i]) {  // empty slots never force a pass
+                any_near |= nq[i];
+                any_far |= !nq[i];
             }
         }
         any_near = __any_sync(0xFFFFFFFFu, any_near);
-        all_near = __all_sync(0xFFFFFFFFu, all_near);
-        const int dist = !any_near ? 0 : (all_near ? 1 : 2);
-        if (mode == 3) {
-            if (dist == 0) k4_tile<3, 0, kQT>(tt, q, nq, sw, swz, cz);
-            else if (dist == 1) k4_tile<3, 1, kQT>(tt, q, nq, sw, swz, cz);
-            else k4_tile<3, 2, kQT>(tt, q, nq, sw, swz, cz);
-        } else if (mode == 0) {
-            if (dist == 0) k4_tile<0, 0, kQT>(tt, q, nq, sw, swz, cz);
-            else k4_tile<0, 2, kQT>(tt, q, nq, sw, swz, cz);
-        } else if (mode == 5) {
-            if (dist == 0) k4_tile<5, 0, kQT>(tt, q, nq, sw, swz, cz);
-            else if (dist == 1) k4_tile<5, 1, kQT>(tt, q, nq, sw, swz, cz);
-            else k4_tile<5, 2, kQT>(tt, q, nq, sw, swz, cz);
-        } else if (mode == 4) {
-            if (dist == 0) k4_tile<4, 0, kQT>(tt, q, nq, sw, swz, cz);
-            else if (dist == 1) k4_tile<4, 1, kQT>(tt, q, nq, sw, swz, cz);
-            else k4_tile<4, 2, kQT>(tt, q, nq, sw, swz, cz);
-        } else if (mode == 1) {
-            if (dist == 0) k4_tile<1, 0, kQT>(tt, q, nq, sw, swz, cz);
-            else if (dist == 1) k4_tile<1, 1, kQT>(tt, q, nq, sw, swz, cz);
-            else k4_tile<1, 2, kQT>(tt, q, nq, sw, swz, cz);
+        any_far = __any_sync(0xFFFFFFFFu, any_far);
+        if (RECIPE) {
+            if (mode == 3) k4_tile<3, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
+            else k4_tile<0, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
         } else {
-            k4_tile<2, 2, kQT>(tt, q, nq, sw, swz, cz);
+            if (mode == 5) k4_tile<5, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
+            else if (mode == 1) k4_tile<1, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
+            else if (mode == 4) k4_tile<4, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
+            else k4_tile<2, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
         }
-#pragma unroll
-        for (int k = 0; k < kPairs; ++k) {
-            float lo, hi;
-            up2(sw[k], lo, hi);
-            SW[2 * k] += static_cast<double>(lo);
-            SW[2 * k + 1] += static_cast<double>(hi);
-            up2(swz[k], lo, hi);
-            float clo, chi;
-            up2(cz[k], clo, chi);
-            SWZ[2 * k] += static_cast<double>(lo) - static_cast<double>(clo);
-            SWZ[2 * k + 1] += static_cast<double>(hi) - static_cast<double>(chi);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0 && it + kStages < ntl) {
-            fence_proxy_async();
-            const size_t tile = t0 + it + kStages;
-            mbar_expect_tx(&bar[st], kTileBytes);
-            bulk_load(stile + st * kTileFloats, a.rec + tile * kTileFloats, kTileBytes, &bar[st]);
+        // release the stage: the last warp done with it refills it, so warps
+        // drift up to kStages tiles apart instead of meeting at a CTA barrier
+        // (a warp with near work on a tile catches up on the far tiles after)
+        __syncwarp();
+        if (lane == 0 && it + kStages < ntl) {
+            __threadfence_block();
+            // counts never reset: the last arrival of round k sees 8k + 7
+            if ((atomicAdd(&done[st], 1u) + 1u) % (kK4Threads / 32) == 0u) {
+                __threadfence_block();
+                fence_proxy_async();
+                const size_t tile = t0 + it + kStages;
+                mbar_expect_tx(&bar[st], kTileBytes);
+                bulk_load(stile + st * kTileFloats, a.rec + tile * kTileFloats, kTileBytes,
+                          &bar[st]);
+            }
         }
     }
 #pragma unroll
     for (int i = 0; i < kQT; ++i) {
         const size_t p = wbase + static_cast<size_t>(i) * 32 + lane;
-        if (p < a.n) a.part[p * a.chunks + chunk] = make_double2(SW[i], SWZ[i]);
+        if (p < q1) a.part[p * a.chunks + chunk] = make_double2(SW[i], SWZ[i]);
     }
+}
+
+// One launch for both classes: CTAs [0, ceil(nG / Q)) take the general
+// region [0, nG) of the visiting order, the rest the recipe region [nG, n)
+// (Q = queries per CTA).  The class counts live on the device (no host sync
+// mid-pipeline); the grid is sized for ceil(n / Q) + 1 CTAs, any surplus
+// CTA exits at once.
+template <int kQT, int kMinBlocks>
+__global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4Args a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* stile = reinterpret_cast<float*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stile + kStages * kTileFloats);
+    unsigned* done = reinterpret_cast<unsigned*>(bar + kStages);
+    constexpr size_t kQ = static_cast<size_t>(kK4Threads) * kQT;
+    const size_t num_a = static_cast<size_t>(a.scan_a[a.n - 1]) + a.flag_a[a.n - 1];
+    const size_t num_g = a.n - num_a;
+    const size_t ctas_g = (num_g + kQ - 1) / kQ;
+    const size_t b = blockIdx.x;
+    if (b >= ctas_g && (b - ctas_g) * kQ >= num_a) return;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&bar[s], 1);
+            done[s] = 0u;
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (b < ctas_g) k4_body<false, kQT>(a, 0, num_g, b, stile, bar, done);
+    else k4_body<true, kQT>(a, num_g, a.n, b - ctas_g, stile, bar, done);
 }
 
 // ------------------------------------------------------------ settle
@@ -723,36 +858,50 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     if (q.n == 0) return;
     const WeightSplit sp = weight_split(d.m);
     const size_t mp = sp.tiles * kWeightTile;
+    // record order: the grid's cells in 8 x 8-cell blocks (compact tiles)
+    DBuf<uint32_t> border;
+    const uint32_t* order = d.order;
+    if (d.order && d.cell_start) {
+        border.alloc(d.m, s);
+        blocked_cell_order(d.cell_start, d.order, d.n_col, d.n_row, d.m, border.get(), s);
+        order = border.get();
+    }
     DBuf<float> rec(sp.tiles * kTileFloats, s);
-    DBuf<float4> tbox(sp.tiles, s);
-    LAUNCH(prep_data_kernel, ceil_div(mp, kThreads), kThreads, 0, s, d.x, d.y, d.z, d.order, d.m,
+    DBuf<float4> tbox(sp.tiles, s), tgeo(sp.tiles, s);
+    LAUNCH(prep_data_kernel, ceil_div(mp, kThreads), kThreads, 0, s, d.x, d.y, d.z, order, d.m,
            mp, f.ox, f.oy, f.inv_scale, std::ldexp(1.0, f.zshift), rec.get());
-    LAUNCH(tile_box_kernel, ceil_div(sp.tiles * 32, kThreads), kThreads, 0, s, rec.get(), d.m,
-           sp.tiles, tbox.get());
-
-    DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), flag_g2(q.n, s), scan_g2(q.n, s), order(q.n, s);
-    DBuf<float4> qhl(q.n, s), qpar(q.n, s);
-    DBuf<double> lshift(q.n, s);
-    LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q,
-           g_alpha4_recipe.load() ? 1 : 0, flag.get(), flag_g2.get());
-    exclusive_scan_u32(flag.get(), scan_a.get(), q.n, s);
-    exclusive_scan_u32(flag_g2.get(), scan_g2.get(), q.n, s);
-    LAUNCH(query_records_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, flag.get(),
-           scan_a.get(), flag_g2.get(), scan_g2.get(), order.get(), qhl.get(), qpar.get(),
-           lshift.get(),
-           times ? times->d_alpha4 : nullptr);
-
-    DBuf<double2> part(q.n * sp.chunks, s);
-    // near / far threshold (unit-box units): beyond it a pair's plain FP32
-    // difference has relative error <= ~8.4e-8 / R_far (AIDW_K4_RFAR to tune)
+    // near threshold R_far (unit-box units): closer (query, tile) pairs take
+    // the hi/lo form (AIDW_K4_RFAR to tune)
     static const float rfar = [] {
         const char* v = std::getenv("AIDW_K4_RFAR");
         return v ? static_cast<float>(std::atof(v)) : 0.05f;
     }();
+    LAUNCH(tile_geo_kernel, ceil_div(sp.tiles * 32, kThreads), kThreads, 0, s, rec.get(), d.m,
+           sp.tiles, rfar * rfar, tbox.get(), tgeo.get());
+    border.release();
+
+    DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), flag_g2(q.n, s), scan_g2(q.n, s), order_q(q.n, s);
+    DBuf<float4> qhl(q.n, s), qpar(q.n, s);
+    DBuf<double> lshift(q.n, s);
+    DBuf<uint32_t> zkey(q.n, s), zpos(q.n, s);
+    LAUNCH(morton_keys_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, zkey.get(),
+           zpos.get());
+    radix_sort_pairs(zkey.get(), zpos.get(), q.n, 32, s);
+    zkey.release();
+    LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f,
+           g_alpha4_recipe.load() ? 1 : 0, zpos.get(), flag.get(), flag_g2.get());
+    exclusive_scan_u32(flag.get(), scan_a.get(), q.n, s);
+    exclusive_scan_u32(flag_g2.get(), scan_g2.get(), q.n, s);
+    LAUNCH(query_records_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, zpos.get(),
+           flag.get(),
+           scan_a.get(), flag_g2.get(), scan_g2.get(), order_q.get(), qhl.get(), qpar.get(),
+           lshift.get(), times ? times->d_alpha4 : nullptr);
+
+    DBuf<double2> part(q.n * sp.chunks, s);
     K4Args ka{rec.get(), sp.tiles, sp.tiles_per_chunk, sp.chunks, qhl.get(), qpar.get(),
-              q.n, part.get(), tbox.get(), rfar * rfar};
-    const size_t smem = kStages * kTileFloats * sizeof(float) +
-                        kStages * sizeof(uint64_t);
+              q.n, flag.get(), scan_a.get(), part.get(), tbox.get(), tgeo.get()};
+    const size_t smem = kStages * kTileFloats * sizeof(float) + kStages * sizeof(uint64_t) +
+                        kStages * sizeof(unsigned);
     // K4 variant: queries per thread x min resident CTAs (AIDW_K4_VARIANT for
     // tuning; default 4 x 3).  Per-query arithmetic is identical in all.
     static const int variant = [] {
@@ -762,7 +911,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     auto launch = [&](auto kernel, int qt) {
         CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-        dim3 grid(ceil_div(q.n, static_cast<size_t>(kK4Threads) * qt), sp.chunks);
+        dim3 grid(ceil_div(q.n, static_cast<size_t>(kK4Threads) * qt) + 1, sp.chunks);
         if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
         LAUNCH(kernel, grid, kK4Threads, smem, s, ka);
     };
@@ -772,7 +921,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
         default: launch(weight_fp32_kernel<4, 3>, 4); break;
     }
     if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
-    LAUNCH(settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order.get(),
+    LAUNCH(settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order_q.get(),
            part.get(), lshift.get(), sp.chunks, d_pred, d_alpha);
 }
 

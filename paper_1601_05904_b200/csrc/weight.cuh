@@ -39,6 +39,10 @@ struct WeightData {
     // FP32 path: record order (cell order of the factor-4 grid over the
     // bbox, so tiles are spatially compact); nullptr = index order
     const uint32_t* order = nullptr;
+    // the grid behind `order` (its CSR cell_start and shape): K4 re-orders
+    // the cells into 8 x 8-cell blocks so each 256-record tile is compact
+    const uint32_t* cell_start = nullptr;
+    int n_col = 0, n_row = 0;
 };
 
 // Optional instrumentation: events recorded around the K4 launch(es) and a
