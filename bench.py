@@ -315,10 +315,18 @@ def main():
     build_ms = statistics.median(s["build_ms"] for s in stats)
     build_bytes = 64 * m + 8 * (m // 4 + 1)  # factor-4 grid: ~m/4 cells (SURVEY §8 grid table)
     a4 = stats[-1]["alpha4_queries"]
-    # MUFU ops per pair of the executed formula mix: 1 (rcp) for queries on
-    # the exact alpha = 4 recipe, 2 (lg2 + ex2) for every other query
-    mufu_per_pair = (a4 * 1 + (n - a4) * 2) / n
-    peak_mix = sms * 16 * f_mhz * 1e6 / mufu_per_pair / 1e9
+    # Pipe roofline of the executed formula mix (K4 far-tile forms):
+    # per SM and clock the FMA pipe retires 128 FP32 ops (FFMA2 = 2) and the
+    # XU pipe 16 MUFU ops; a class is bound by the slower of the two.
+    #   recipe (alpha == 4): 3 (d2) + 1 (d2^2) + 2.5 (pair/single sums) = 6.5
+    #     FP32 + 0.75 MUFU per pair (two of every four points share one rcp)
+    #   general: G1 6 FP32 + 2 MUFU (lg2, ex2), G2 15 FP32 + 1 MUFU (ex2 as a
+    #     degree-6 polynomial); G1 / G2 split ~1:1 by coordinate hash
+    clk_recipe = max(6.5 / 128, 0.75 / 16)
+    clk_general = max(0.5 * (6 + 15) / 128, 0.5 * (2 + 1) / 16)
+    clk_mix = (a4 * clk_recipe + (n - a4) * clk_general) / n
+    peak_mix = sms * f_mhz * 1e6 / clk_mix / 1e9
+    peak_general = sms * f_mhz * 1e6 / clk_general / 1e9
 
     # general-alpha path forced (every query on exp2/log2), reported separately
     A.set_alpha4_recipe(False)
@@ -364,19 +372,23 @@ def main():
                        "parallelism": f"query-sharded x{world}, data replicated (NCCL broadcast)",
                        "l2": "flushed between timed steps (256 MiB write)",
                        "device": name, "sms": sms},
-            "roofline": {"bound": "mufu", "kernel": "weight_fp32_kernel (K4)",
+            "roofline": {"bound": "fp32+mufu pipes", "kernel": "weight_fp32_kernel (K4)",
                          "achieved": achieved, "peak": peak_mix, "unit": "Gpair/s",
                          "frac": achieved / peak_mix, "traffic": k4_traffic(cfg),
-                         "peak_def": f"{sms} SMs x 16 MUFU/clk x {f_mhz:.0f} MHz ({pk['source']} "
-                                     f"sm_max_mhz) / {mufu_per_pair:.4f} MUFU per pair (executed "
-                                     f"mix: 1 for alpha=4 recipe queries, 2 for exp2/log2)",
-                         "mufu_per_pair": mufu_per_pair,
+                         "peak_def": f"{sms} SMs x {f_mhz:.0f} MHz ({pk['source']} sm_max_mhz) / "
+                                     f"{clk_mix:.4f} SM-clk per pair: executed mix of the "
+                                     f"alpha=4 recipe ({a4} queries; FMA-bound 6.5 FP32 + "
+                                     f"0.75 MUFU) and general alpha (MUFU-bound 10.5 FP32 + "
+                                     f"1.5 MUFU) far-tile forms; 128 FP32 + 16 MUFU per SM-clk",
                          "frac_vs_2mufu_roofline": achieved / peak_gpairs,
                          "alpha4_recipe_queries": a4, "pairs_per_launch": pairs,
                          "k4_ms": k4_ms},
-            "roofline_general_alpha": {"bound": "mufu", "achieved": pairs / (k4g_ms / 1e3) / 1e9,
-                                       "peak": peak_gpairs, "unit": "Gpair/s",
-                                       "frac": pairs / (k4g_ms / 1e3) / 1e9 / peak_gpairs,
+            "roofline_general_alpha": {"bound": "fp32+mufu pipes (MUFU-bound)",
+                                       "achieved": pairs / (k4g_ms / 1e3) / 1e9,
+                                       "peak": peak_general, "unit": "Gpair/s",
+                                       "frac": pairs / (k4g_ms / 1e3) / 1e9 / peak_general,
+                                       "frac_vs_2mufu_roofline":
+                                           pairs / (k4g_ms / 1e3) / 1e9 / peak_gpairs,
                                        "k4_ms": k4g_ms},
             "stages": {
                 "build_ms": build_ms,

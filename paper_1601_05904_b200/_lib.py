@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libaidw_b200.so")
+# AIDW_LIB_PATH: an alternative build of the same library (kernel-tuning
+# experiments); the default is the in-tree build
+LIB_PATH = os.environ.get("AIDW_LIB_PATH") or os.path.join(HERE, "lib", "libaidw_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "aidw_capi.h")
 
 AIDW_OK = 0

@@ -43,7 +43,10 @@ namespace aidwb {
 namespace {
 
 constexpr int kK4Threads = 256;
-constexpr int kStages = 4;
+#ifndef AIDW_K4_STAGES
+#define AIDW_K4_STAGES 4
+#endif
+constexpr int kStages = AIDW_K4_STAGES;
 constexpr int kMaxChunks = 16;
 constexpr int kTileFloats = 9 * kWeightTile;  // SoA tile, 9 components (see kComps)
 
@@ -170,7 +173,7 @@ __global__ void tile_geo_kernel(float* __restrict__ rec, size_t m, size_t tiles,
     const float cx = 0.5f * (x0 + x1), cy = 0.5f * (y0 + y1);
     const float gx = x1 - x0, gy = y1 - y0;
     const bool partial = (tile + 1) * kWeightTile > m;
-    const float thr2 = partial ? INFINITY : fmaxf(rfar2, 1.001f * fmaf(gx, gx, gy * gy));
+    const float thr2 = partial ? INFINITY : fmaxf(fmaxf(rfar2, 1.0e-8f), 1.001f * fmaf(gx, gx, gy * gy));
     if (lane == 0) {
         box[tile] = make_float4(x0, y0, x1, y1);
         geo[tile] = make_float4(cx, cy, thr2, 0.0f);
@@ -485,7 +488,8 @@ __device__ __forceinline__ f2 general_w(f2 d2, const QState<QT>& q, int r) {
 // pair; sums plain (far pairs carry a small weight share or average out).
 // Recipe modes pair points 4j and 4j+1 on one reciprocal,
 //   w0 + w1 = (a0 + a1) rcp(a0 a1),  w0 z0 + w1 z1 = (a1 z0 + a0 z1) rcp(a0 a1),
-// a = (d2 s)^2 — 6.5 FP32 ops + 0.75 MUFU per pair, balancing the FMA pipe
+// a = d2^2 (far d2 >= 1e-8: no range scaling) — 6.5 FP32 ops + 0.75 MUFU per
+// pair, balancing the FMA pipe
 // (128 lanes / clk / SM) against MUFU (16 / clk / SM).
 template <int MODE, int QT>
 __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState<QT>& q,
@@ -501,28 +505,28 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
         const float4 Z = *reinterpret_cast<const float4*>(t + kZH * kWeightTile + j);
 #pragma unroll
         for (int r = 0; r < kPairs; ++r) {
-            f2 d0 = add2(fma2(bc2(Y.x), fy[r], fma2(bc2(X.x), fx[r], fq[r])), bc2(P.x));
-            f2 d1 = add2(fma2(bc2(Y.y), fy[r], fma2(bc2(X.y), fx[r], fq[r])), bc2(P.y));
-            f2 d2 = add2(fma2(bc2(Y.z), fy[r], fma2(bc2(X.z), fx[r], fq[r])), bc2(P.z));
-            f2 d3 = add2(fma2(bc2(Y.w), fy[r], fma2(bc2(X.w), fx[r], fq[r])), bc2(P.w));
-            if (MODE == 3 || MODE == 0) {
-                if (MODE == 0) {
-                    d0 = mul2(d0, q.s[r]);
-                    d1 = mul2(d1, q.s[r]);
-                    d2 = mul2(d2, q.s[r]);
-                    d3 = mul2(d3, q.s[r]);
-                }
+            const f2 d0 = add2(fma2(bc2(Y.x), fy[r], fma2(bc2(X.x), fx[r], fq[r])), bc2(P.x));
+            const f2 d1 = add2(fma2(bc2(Y.y), fy[r], fma2(bc2(X.y), fx[r], fq[r])), bc2(P.y));
+            const f2 d2 = add2(fma2(bc2(Y.z), fy[r], fma2(bc2(X.z), fx[r], fq[r])), bc2(P.z));
+            const f2 d3 = add2(fma2(bc2(Y.w), fy[r], fma2(bc2(X.w), fx[r], fq[r])), bc2(P.w));
+            if (MODE == 3) {
                 const f2 a0 = mul2(d0, d0), a1 = mul2(d1, d1);
                 const f2 a2 = mul2(d2, d2), a3 = mul2(d3, d3);
                 const f2 r01 = rcp2(mul2(a0, a1));
                 sw[r] = fma2(r01, add2(a0, a1), sw[r]);
                 swz[r] = fma2(r01, fma2(a1, bc2(Z.x), mul2(a0, bc2(Z.y))), swz[r]);
+#if AIDW_K4_ALLPAIRS
+                const f2 r23 = rcp2(mul2(a2, a3));
+                sw[r] = fma2(r23, add2(a2, a3), sw[r]);
+                swz[r] = fma2(r23, fma2(a3, bc2(Z.z), mul2(a2, bc2(Z.w))), swz[r]);
+#else
                 const f2 w2 = rcp2(a2);
                 sw[r] = add2(sw[r], w2);
                 swz[r] = fma2(w2, bc2(Z.z), swz[r]);
                 const f2 w3 = rcp2(a3);
                 sw[r] = add2(sw[r], w3);
                 swz[r] = fma2(w3, bc2(Z.w), swz[r]);
+#endif
             } else {
                 const f2 w0 = general_w<MODE, QT>(d0, q, r);
                 sw[r] = add2(sw[r], w0);
@@ -614,14 +618,24 @@ __device__ __forceinline__ void k4_tile(const float* __restrict__ t, const QStat
                 sw[r] = swz[r] = 0ull;
             }
         }
-        k4_far<MODE, QT>(t, q, fx, fy, fq, sw, swz);
+        // far pairs never need the recipe's range scaling (d2 >= the near
+        // threshold >= 1e-8): mode 0 runs the s-free form and rescales the
+        // tile sums by s^-2 (a power of two: exact)
+        k4_far<MODE == 0 ? 3 : MODE, QT>(t, q, fx, fy, fq, sw, swz);
 #pragma unroll
         for (int r = 0; r < kPairs; ++r) {
             float w0, w1, z0, z1;
             up2(sw[r], w0, w1);
             up2(swz[r], z0, z1);
-            if (!nq[2 * r]) SW[2 * r] += w0, SWZ[2 * r] += z0;
-            if (!nq[2 * r + 1]) SW[2 * r + 1] += w1, SWZ[2 * r + 1] += z1;
+            double m0 = 1.0, m1 = 1.0;
+            if (MODE == 0) {
+                float s0, s1;
+                up2(q.s[r], s0, s1);
+                m0 = 1.0 / (static_cast<double>(s0) * s0);
+                m1 = 1.0 / (static_cast<double>(s1) * s1);
+            }
+            if (!nq[2 * r]) SW[2 * r] += w0 * m0, SWZ[2 * r] += z0 * m0;
+            if (!nq[2 * r + 1]) SW[2 * r + 1] += w1 * m1, SWZ[2 * r + 1] += z1 * m1;
         }
     }
     if (any_near) {
@@ -874,7 +888,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     // the hi/lo form (AIDW_K4_RFAR to tune)
     static const float rfar = [] {
         const char* v = std::getenv("AIDW_K4_RFAR");
-        return v ? static_cast<float>(std::atof(v)) : 0.05f;
+        return v ? static_cast<float>(std::atof(v)) : 0.02f;
     }();
     LAUNCH(tile_geo_kernel, ceil_div(sp.tiles * 32, kThreads), kThreads, 0, s, rec.get(), d.m,
            sp.tiles, rfar * rfar, tbox.get(), tgeo.get());
@@ -903,7 +917,8 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     const size_t smem = kStages * kTileFloats * sizeof(float) + kStages * sizeof(uint64_t) +
                         kStages * sizeof(unsigned);
     // K4 variant: queries per thread x min resident CTAs (AIDW_K4_VARIANT for
-    // tuning; default 4 x 3).  Per-query arithmetic is identical in all.
+    // tuning; default 4 x 2: 124 registers, no spills — faster than 4 x 3 at
+    // 80 registers).  Per-query arithmetic is identical in all.
     static const int variant = [] {
         const char* v = std::getenv("AIDW_K4_VARIANT");
         return v ? std::atoi(v) : 0;
@@ -916,9 +931,9 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
         LAUNCH(kernel, grid, kK4Threads, smem, s, ka);
     };
     switch (variant) {
-        case 1: launch(weight_fp32_kernel<4, 2>, 4); break;
+        case 1: launch(weight_fp32_kernel<4, 3>, 4); break;
         case 2: launch(weight_fp32_kernel<2, 4>, 2); break;
-        default: launch(weight_fp32_kernel<4, 3>, 4); break;
+        default: launch(weight_fp32_kernel<4, 2>, 4); break;
     }
     if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
     LAUNCH(settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order_q.get(),
