@@ -5,7 +5,8 @@
 //
 // One thread per query; queries are visited in cell-sorted order (radix
 // sort in grid_build.cu) so a warp's 32 queries scan overlapping cell
-// blocks and the candidate loads hit L1.  The search is the reference's:
+// blocks and the candidate loads hit L1; each thread walks its cells as one
+// level block row by row (a row segment of cells is contiguous in memory).  The search is the reference's:
 // expansion level = smallest L0 whose clipped (2L0+1)^2 block holds >= k
 // points, plus one; scan that block; widen ring by ring until
 // kth <= (L*w)^2 (1 - 1e-9) or the block covers the grid.  The block is
@@ -159,52 +160,6 @@ __device__ __forceinline__ double cell_lower_d2(const GridGeom& g, double fx, do
     return (dx * dx + dy * dy) * w2 * (1.0 - 1.0e-9);
 }
 
-template <class TopK>
-__device__ __forceinline__ void scan_cell(const KnnArgs& a, TopK& t, double qx, double qy,
-                                          double fx, double fy, double w2, int c, int r,
-                                          uint32_t& snap, unsigned long long& scanned) {
-    if (t.full()) {
-        const double lb = cell_lower_d2(a.g, fx, fy, w2, c, r);
-        if (lb > fmax(t.kth(), a.snap_sq)) return;  // every point is strictly worse
-    }
-    const size_t id = static_cast<size_t>(r) * static_cast<size_t>(a.g.n_col) + c;
-    const uint32_t b = __ldg(a.cell_start + id);
-    const uint32_t e = __ldg(a.cell_start + id + 1);
-    scanned += e - b;
-    for (uint32_t s = b; s < e; ++s) {
-        const double2 pxy = __ldg(a.sorted_xy + s);
-        const double cd = dsq_rn(qx, qy, pxy.x, pxy.y);
-        if (cd <= a.snap_sq) {
-            const uint32_t cid = __ldg(a.sorted_ids + s);
-            snap = cid < snap ? cid : snap;
-        }
-        if (t.admits(cd)) t.insert(cd, __ldg(a.sorted_ids + s));
-    }
-}
-
-// The cells at Chebyshev distance r from (col, row), clipped to the grid.
-template <class TopK>
-__device__ __forceinline__ void scan_ring(const KnnArgs& a, TopK& t, double qx, double qy,
-                                          double fx, double fy, double w2, int col, int row,
-                                          int r, uint32_t& snap, unsigned long long& scanned) {
-    const int n_col = a.g.n_col, n_row = a.g.n_row;
-    if (r == 0) {
-        scan_cell(a, t, qx, qy, fx, fy, w2, col, row, snap, scanned);
-        return;
-    }
-    const int c0 = col - r < 0 ? 0 : col - r, c1 = col + r > n_col - 1 ? n_col - 1 : col + r;
-    const int r0 = row - r + 1 < 0 ? 0 : row - r + 1;
-    const int r1 = row + r - 1 > n_row - 1 ? n_row - 1 : row + r - 1;
-    if (row - r >= 0)
-        for (int c = c0; c <= c1; ++c) scan_cell(a, t, qx, qy, fx, fy, w2, c, row - r, snap, scanned);
-    if (row + r <= n_row - 1)
-        for (int c = c0; c <= c1; ++c) scan_cell(a, t, qx, qy, fx, fy, w2, c, row + r, snap, scanned);
-    if (col - r >= 0)
-        for (int rr = r0; rr <= r1; ++rr) scan_cell(a, t, qx, qy, fx, fy, w2, col - r, rr, snap, scanned);
-    if (col + r <= n_col - 1)
-        for (int rr = r0; rr <= r1; ++rr) scan_cell(a, t, qx, qy, fx, fy, w2, col + r, rr, snap, scanned);
-}
-
 __device__ __forceinline__ size_t rect_count(const KnnArgs& a, int c0, int c1, int r0, int r1) {
     size_t total = 0;
     for (int r = r0; r <= r1; ++r) {
@@ -285,6 +240,61 @@ __device__ __forceinline__ void finish_query(const KnnArgs& a, TopK& t, size_t p
     }
 }
 
+// Points of row rr, cells [c0, c1] (clipped to the grid): contiguous in the
+// cell-sorted arrays (row-major cells), so one cell_start round trip and one
+// loop cover the whole segment.  Once the buffer is full the segment is
+// trimmed to the cells whose padded rectangle can hold a point with
+// d2 <= max(kth, snap_sq) — the per-cell lower bound of cell_lower_d2 solved
+// for the column range, widened by a further safety margin (trimming only
+// ever keeps more cells than the exact test, so results are unchanged).
+// The next candidate's coordinates and id are loaded one iteration ahead.
+template <class TopK>
+__device__ __forceinline__ void scan_row(const KnnArgs& a, TopK& t, double qx, double qy,
+                                         double fx, double fy, double w2, int rr, int c0, int c1,
+                                         uint32_t& snap, unsigned long long& scanned) {
+    const int n_col = a.g.n_col, n_row = a.g.n_row;
+    if (t.full()) {
+        const double inf = __longlong_as_double(0x7FF0000000000000ll);
+        const double pad = 1.0e-7;
+        const double thr = fmax(t.kth(), a.snap_sq);
+        const double y0 = rr == 0 ? -inf : rr - pad, y1 = rr == n_row - 1 ? inf : rr + 1 + pad;
+        const double dy = fmax(0.0, fmax(y0 - fy, fy - y1));
+        const double room = thr / (w2 * (1.0 - 1.0e-9)) - dy * dy;  // dx^2 budget, cell units
+        if (room < 0.0) return;  // the whole row is strictly worse
+        const double h = sqrt(room) * (1.0 + 1.0e-9) + 1.0e-9;
+        // cell c is kept iff c - pad - fx <= h and fx - (c + 1 + pad) <= h;
+        // the edge cells are unbounded outward (keep them on their open side)
+        const double lo = floor(fx - h - pad - 1.0), hi = floor(fx + h + pad);
+        int k0 = lo < c0 ? c0 : (lo > c1 ? c1 + 1 : static_cast<int>(lo));
+        int k1 = hi > c1 ? c1 : (hi < c0 ? c0 - 1 : static_cast<int>(hi));
+        if (c0 == 0 && k1 < 0) k1 = 0;
+        if (c1 == n_col - 1 && k0 > n_col - 1) k0 = n_col - 1;
+        c0 = k0, c1 = k1;
+        if (c0 > c1) return;
+    }
+    const size_t base = static_cast<size_t>(rr) * static_cast<size_t>(n_col);
+    uint32_t s = __ldg(a.cell_start + base + c0);
+    const uint32_t e = __ldg(a.cell_start + base + c1 + 1);
+    scanned += e - s;
+    if (s >= e) return;
+    double2 pxy = __ldg(a.sorted_xy + s);
+    uint32_t pid = __ldg(a.sorted_ids + s);
+    while (true) {
+        const double2 cxy = pxy;
+        const uint32_t cid = pid;
+        const bool more = ++s < e;
+        if (more) {
+            pxy = __ldg(a.sorted_xy + s);
+            pid = __ldg(a.sorted_ids + s);
+        }
+        const double cd = dsq_rn(qx, qy, cxy.x, cxy.y);
+        if (cd <= a.snap_sq) snap = cid < snap ? cid : snap;
+        if (t.admits(cd)) t.insert(cd, cid);
+        if (!more) break;
+    }
+}
+
+// One thread per query.
 template <class TopK>
 __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
     const size_t pos = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -315,15 +325,23 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
         TopK t;
         t.init(a.k_eff, a.scratch_d + pos * a.k_eff, a.scratch_id + pos * a.k_eff);
         uint32_t snap = kNoId;
-        // query in cell units, for the per-cell lower bound
+        // query in cell units, for the lower bounds
         const double fx = __ddiv_rn(__dsub_rn(qx, a.g.min_x), a.g.cell_width);
         const double fy = __ddiv_rn(__dsub_rn(qy, a.g.min_y), a.g.cell_width);
         const double w2 = __dmul_rn(a.g.cell_width, a.g.cell_width);
-        // The reference scans the whole level block at once; scanning it ring
-        // by ring from the query's cell and skipping cells that cannot hold a
-        // point below the current k-th yields the same k smallest (d2, idx)
-        // of the block, hence identical stop decisions and results.
-        for (int r = 0; r <= level; ++r) scan_ring(a, t, qx, qy, fx, fy, w2, col, row, r, snap, scanned);
+        // The reference scans the whole level block at once; scanning it row
+        // by row outward from the query's row and trimming each row to the
+        // cells that can still hold a point below the current k-th yields the
+        // same k smallest (d2, idx) of the block, hence identical stop
+        // decisions and results.
+        {
+            const int c0 = imax(0, col - level), c1 = imin(n_col - 1, col + level);
+            for (int d = 0; d <= 2 * level; ++d) {
+                const int rr = row + ((d & 1) ? -((d + 1) >> 1) : (d >> 1));
+                if (rr < 0 || rr >= n_row) continue;
+                scan_row(a, t, qx, qy, fx, fy, w2, rr, c0, c1, snap, scanned);
+            }
+        }
         // ring widening (knn.hpp:234-247, scan_ring :175-194)
         while (true) {
             const bool covers = col - level <= 0 && row - level <= 0 &&
@@ -333,7 +351,18 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
             const double bound = __dmul_rn(__dmul_rn(reach, reach), a.ring_margin);
             if (t.full() && t.kth() <= bound) break;
             ++level;
-            scan_ring(a, t, qx, qy, fx, fy, w2, col, row, level, snap, scanned);
+            const int r = level;
+            const int c0 = imax(0, col - r), c1 = imin(n_col - 1, col + r);
+            if (row - r >= 0) scan_row(a, t, qx, qy, fx, fy, w2, row - r, c0, c1, snap, scanned);
+            if (row + r <= n_row - 1)
+                scan_row(a, t, qx, qy, fx, fy, w2, row + r, c0, c1, snap, scanned);
+            const int r0 = imax(0, row - r + 1), r1 = imin(n_row - 1, row + r - 1);
+            if (col - r >= 0)
+                for (int rr = r0; rr <= r1; ++rr)
+                    scan_row(a, t, qx, qy, fx, fy, w2, rr, col - r, col - r, snap, scanned);
+            if (col + r <= n_col - 1)
+                for (int rr = r0; rr <= r1; ++rr)
+                    scan_row(a, t, qx, qy, fx, fy, w2, rr, col + r, col + r, snap, scanned);
         }
         if (a.ref_candidates) {  // what the reference scanned: the final-level block
             ref_scanned = rect_count(a, imax(0, col - level), imin(n_col - 1, col + level),
