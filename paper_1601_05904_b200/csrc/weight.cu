@@ -151,7 +151,7 @@ __global__ void prep_data_kernel(const double* __restrict__ x, const double* __r
 // ulp of d2 (~1e-7 relative), against ~1e-6 for plain hi differences.
 // Partial (padded) tiles are always NEAR.
 __global__ void tile_geo_kernel(float* __restrict__ rec, size_t m, size_t tiles, float rfar2,
-                                float4* __restrict__ box, float4* __restrict__ geo) {
+                                float diagf2, float4* __restrict__ box, float4* __restrict__ geo) {
     const size_t tile = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (tile >= tiles) return;
@@ -173,7 +173,8 @@ __global__ void tile_geo_kernel(float* __restrict__ rec, size_t m, size_t tiles,
     const float cx = 0.5f * (x0 + x1), cy = 0.5f * (y0 + y1);
     const float gx = x1 - x0, gy = y1 - y0;
     const bool partial = (tile + 1) * kWeightTile > m;
-    const float thr2 = partial ? INFINITY : fmaxf(fmaxf(rfar2, 1.0e-8f), 1.001f * fmaf(gx, gx, gy * gy));
+    const float thr2 =
+        partial ? INFINITY : fmaxf(fmaxf(rfar2, 1.0e-8f), 1.001f * diagf2 * fmaf(gx, gx, gy * gy));
     if (lane == 0) {
         box[tile] = make_float4(x0, y0, x1, y1);
         geo[tile] = make_float4(cx, cy, thr2, 0.0f);
@@ -213,12 +214,12 @@ constexpr double kRecipeLowD2 = 1.0e-9;
 // sharding, order or GPU count, and frame-relative, so translating the whole
 // problem (acceptance criterion 5, 1e-9) does not re-class it.  Half / half
 // balances the MUFU and FMA pipes.
-__device__ __forceinline__ bool poly_class(float xh, float yh) {
+__device__ __forceinline__ bool poly_class(float xh, float yh, unsigned g2_threshold) {
     unsigned h = static_cast<unsigned>(__float_as_int(xh)) * 0x9E3779B1u;
     h ^= static_cast<unsigned>(__float_as_int(yh)) * 0x85EBCA77u;
     h ^= h >> 15;
     h *= 0xC2B2AE3Du;
-    return (h >> 31) != 0;
+    return h < g2_threshold;
 }
 
 // K4 visiting order: positions sorted along a Morton (Z) curve of the
@@ -248,7 +249,7 @@ __global__ void morton_keys_kernel(const WeightQueries q, WeightFrame f, uint32_
 
 // Flags by Morton rank j (p = zpos[j]).
 __global__ void class_flags_kernel(const WeightQueries q, WeightFrame f, int recipe,
-                                   const uint32_t* __restrict__ zpos,
+                                   unsigned g2_threshold, const uint32_t* __restrict__ zpos,
                                    uint32_t* __restrict__ flag_a, uint32_t* __restrict__ flag_g2) {
     const size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= q.n) return;
@@ -259,7 +260,7 @@ __global__ void class_flags_kernel(const WeightQueries q, WeightFrame f, int rec
     flag_a[j] = a ? 1u : 0u;
     const float xh = __double2float_rn((q.qx[qi] - f.ox) * f.inv_scale);
     const float yh = __double2float_rn((q.qy[qi] - f.oy) * f.inv_scale);
-    flag_g2[j] = (!a && poly_class(xh, yh)) ? 1u : 0u;
+    flag_g2[j] = (!a && poly_class(xh, yh, g2_threshold)) ? 1u : 0u;
 }
 
 // 3-way partition (general G1/G2 interleaved, then A) fused with the
@@ -888,10 +889,15 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     // the hi/lo form (AIDW_K4_RFAR to tune)
     static const float rfar = [] {
         const char* v = std::getenv("AIDW_K4_RFAR");
-        return v ? static_cast<float>(std::atof(v)) : 0.02f;
+        return v ? static_cast<float>(std::atof(v)) : 0.01f;
+    }();
+    // far form needs box distance >= diagf * tile diagonal (AIDW_K4_DIAGF)
+    static const float diagf = [] {
+        const char* v = std::getenv("AIDW_K4_DIAGF");
+        return v ? static_cast<float>(std::atof(v)) : 0.5f;
     }();
     LAUNCH(tile_geo_kernel, ceil_div(sp.tiles * 32, kThreads), kThreads, 0, s, rec.get(), d.m,
-           sp.tiles, rfar * rfar, tbox.get(), tgeo.get());
+           sp.tiles, rfar * rfar, diagf * diagf, tbox.get(), tgeo.get());
     border.release();
 
     DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), flag_g2(q.n, s), scan_g2(q.n, s), order_q(q.n, s);
@@ -902,8 +908,15 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
            zpos.get());
     radix_sort_pairs(zkey.get(), zpos.get(), q.n, 32, s);
     zkey.release();
+    // share of general-alpha queries on the FMA-pipe exp2 (G2); the rest of
+    // a G1 / G2 interleave runs as all-G2 warps (AIDW_K4_G2 to tune)
+    static const unsigned g2_threshold = [] {
+        const char* v = std::getenv("AIDW_K4_G2");
+        const double share = v ? std::atof(v) : 0.5;
+        return static_cast<unsigned>(std::fmin(share, 1.0) * 4294967295.0);
+    }();
     LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f,
-           g_alpha4_recipe.load() ? 1 : 0, zpos.get(), flag.get(), flag_g2.get());
+           g_alpha4_recipe.load() ? 1 : 0, g2_threshold, zpos.get(), flag.get(), flag_g2.get());
     exclusive_scan_u32(flag.get(), scan_a.get(), q.n, s);
     exclusive_scan_u32(flag_g2.get(), scan_g2.get(), q.n, s);
     LAUNCH(query_records_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, zpos.get(),
