@@ -331,7 +331,7 @@ struct K4Args {
     size_t n;
     const uint32_t* flag_a;  // class counts: A = scan_a[n-1] + flag_a[n-1]
     const uint32_t* scan_a;
-    double2* part;            // n * chunks, by visiting position
+    double2* part;            // chunks x n (chunk-major: coalesced), by visiting position
     const float4* tile_box;   // hi-coordinate box of every tile's real records
     const float4* tile_geo;   // {cx, cy, near threshold^2, 0}
 };
@@ -780,7 +780,7 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
 #pragma unroll
     for (int i = 0; i < kQT; ++i) {
         const size_t p = wbase + static_cast<size_t>(i) * 32 + lane;
-        if (p < q1) a.part[p * a.chunks + chunk] = make_double2(SW[i], SWZ[i]);
+        if (p < q1) a.part[static_cast<size_t>(chunk) * a.n + p] = make_double2(SW[i], SWZ[i]);
     }
 }
 
@@ -831,7 +831,7 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
     } else {
         double sw = 0.0, swz = 0.0;
         for (unsigned c = 0; c < chunks; ++c) {
-            const double2 v = part[static_cast<size_t>(i) * chunks + c];
+            const double2 v = part[static_cast<size_t>(c) * q.n + i];
             sw += v.x;
             swz += v.y;
         }
