@@ -187,6 +187,31 @@ int aidw_compute_bbox_device(const double* d_dx, const double* d_dy, size_t m,
                              const double* d_qx, const double* d_qy, size_t n, double* out,
                              void* stream, aidw_error* err);
 
+/* ------------------------------------------------------------ raster (cmd_raster) */
+/* cmd_raster's lattice (cli.hpp:496-507) generated on the device: rows
+ * [row0, row0 + rows) of the nx x ny lattice over bbox = {min_x, min_y,
+ * max_x, max_y}, row-major, northernmost row first (row 0).  Device
+ * buffers of nx * rows doubles; `stream` as aidw_run_pipeline_device. */
+int aidw_raster_lattice_device(size_t nx, size_t ny, const double* bbox, size_t row0,
+                               size_t rows, double* d_xs, double* d_ys, void* stream,
+                               aidw_error* err);
+
+/* The compute part of cli::cmd_raster (cli.hpp:484-524) without file I/O:
+ * data (host buffers) -> lattice over bbox(data) generated in HBM ->
+ * the fused run_pipeline -> raster_out[nx * ny] (north-first, row-major;
+ * = Raster::values).  alpha_out may be NULL; bbox_out (4 doubles, may be
+ * NULL) receives the lattice box (Raster::xllcorner = bbox_out[0],
+ * yllcorner = bbox_out[1], cellsize = (max_x - min_x) / nx). */
+int aidw_run_raster(const double* dx, const double* dy, const double* dz, size_t m, size_t nx,
+                    size_t ny, const aidw_run_config* cfg, double* raster_out, double* alpha_out,
+                    double* bbox_out, aidw_run_stats* stats, aidw_error* err);
+
+/* write_raster_asc (io.hpp:199-221): the ESRI ASCII grid, byte-identical to
+ * the reference writer ("%.17g" values), formatted on all host threads. */
+int aidw_write_raster_asc(const char* path, size_t ncols, size_t nrows, double xllcorner,
+                          double yllcorner, double cellsize, const double* values,
+                          aidw_error* err);
+
 /* ------------------------------------------------------------ synthetic inputs */
 /* generate_random_points / generate_random_queries — generate.hpp:45-95
  * (mt19937_64, 53-bit unit doubles; rule 0 uniform, 1 planar, 2 radial). */

@@ -380,3 +380,30 @@ def ref_run_pipeline(dx, dy, dz, qx, qy, mode=1, engine=0, variant=1, k=15, r_mi
 
 def ref_hardware_threads():
     return int(ref().ref_hardware_threads())
+
+
+def raster_lattice(nx, ny, bbox):
+    """cmd_raster lattice (cli.hpp:495-507), C restatement."""
+    xs, ys = np.empty(nx * ny), np.empty(nx * ny)
+    bb = _d(bbox)
+    _check(orc().orc_raster_lattice(C.c_size_t(nx), C.c_size_t(ny), _p(bb, _dp), _p(xs, _dp),
+                                    _p(ys, _dp)))
+    return xs, ys
+
+
+def ref_cmd_raster(dx, dy, dz, nx, ny, k=15, workers=0, tmpdir="/tmp"):
+    """The reference's own cli::cmd_raster (data written to CSV by the
+    reference writer, read back by its parser, raster written by its
+    write_raster_asc).  Returns (values (nrows*ncols,), meta dict, asc path)."""
+    import os
+    dx, dy, dz = _d(dx), _d(dy), _d(dz)
+    csv = os.path.join(tmpdir, f"aidw_ref_raster_{os.getpid()}.csv").encode()
+    asc = os.path.join(tmpdir, f"aidw_ref_raster_{os.getpid()}.asc").encode()
+    vals, meta = np.empty(nx * ny), np.empty(5)
+    m = _msg()
+    _check(ref().ref_cmd_raster(_p(dx, _dp), _p(dy, _dp), _p(dz, _dp), C.c_size_t(dx.size),
+                                C.c_size_t(nx), C.c_size_t(ny), C.c_int(k), C.c_int(workers), csv,
+                                asc, _p(vals, _dp), _p(meta, _dp), m, C.c_size_t(_MSG)), -1,
+           m.value)
+    return vals, dict(zip(("ncols", "nrows", "xllcorner", "yllcorner", "cellsize"), meta)), \
+        asc.decode()

@@ -663,3 +663,22 @@ int orc_generate_clustered(size_t count, int blobs, double sigma, uint64_t cente
     free(cy);
     return ORC_OK;
 }
+
+/* cmd_raster's query lattice (cli.hpp:495-507): nx x ny cell centres over
+ * the data bbox, northernmost row first, row-major:
+ *   sx = W / nx, sy = H / ny,
+ *   x = min_x + (c + 0.5) sx,  y = min_y + ((ny - 1 - r) + 0.5) sy. */
+int orc_raster_lattice(size_t nx, size_t ny, const double* bbox, double* xs, double* ys) {
+    if (nx < 1 || ny < 1) return ORC_INVALID;
+    const double sx = (bbox[2] - bbox[0]) / (double)nx;
+    const double sy = (bbox[3] - bbox[1]) / (double)ny;
+    size_t i = 0;
+    for (size_t r = 0; r < ny; ++r) {
+        const double y = bbox[1] + ((double)(ny - 1 - r) + 0.5) * sy;
+        for (size_t c = 0; c < nx; ++c, ++i) {
+            xs[i] = bbox[0] + ((double)c + 0.5) * sx;
+            ys[i] = y;
+        }
+    }
+    return 0;
+}

@@ -270,6 +270,34 @@ int ref_predict_all(const double* dx, const double* dy, const double* dz, std::s
     }
 }
 
+// cli::cmd_raster (cli.hpp:484-524) end to end: the data set goes through
+// the reference's CSV writer and parser, the raster through its
+// write_raster_asc.  meta = {ncols, nrows, xllcorner, yllcorner, cellsize}.
+int ref_cmd_raster(const double* dx, const double* dy, const double* dz, std::size_t m,
+                   std::size_t nx, std::size_t ny, int k, int workers, const char* csv_path,
+                   const char* asc_path, double* values, double* meta, char* msg,
+                   std::size_t cap) {
+    try {
+        aidw::write_data_csv(csv_path, make_set(dx, dy, dz, m));
+        aidw::cli::RunConfig cfg;
+        const double levels[5] = {0.5, 1.0, 2.0, 3.0, 4.0};  // types.hpp defaults
+        cfg.params = make_params(k, 0.0, 2.0, levels, 0.0);
+        cfg.workers = workers;
+        cfg.data_path = csv_path;
+        cfg.out_path = asc_path;
+        const aidw::cli::RasterOutcome out = aidw::cli::cmd_raster(cfg, nx, ny);
+        std::memcpy(values, out.raster.values.data(), nx * ny * sizeof(double));
+        meta[0] = static_cast<double>(out.raster.ncols);
+        meta[1] = static_cast<double>(out.raster.nrows);
+        meta[2] = out.raster.xllcorner;
+        meta[3] = out.raster.yllcorner;
+        meta[4] = out.raster.cellsize;
+        return 0;
+    } catch (const std::exception& e) {
+        return classify(e, msg, cap);
+    }
+}
+
 int ref_hardware_threads() { return aidw::resolve_workers(0); }
 
 }  // extern "C"

@@ -9,9 +9,10 @@ reference API over that C-ABI (api.py) plus the ctypes binding (_lib.py).
 from .api import (  # noqa: F401
     AidwParams, AidwRuntimeError, BoundingBox, CudaError, DomainError, GridConfig, GridIndex,
     InterpolationResult, InvalidArgument, KnnStageResult, OutOfRange, PipelineOutcome, PointSet,
-    RunConfig, aidw_predict_all, build_index, choose_cell_width, compute_bbox, compute_bbox_device,
-    device_info, generate_clustered, generate_random_points, generate_random_queries,
-    idw_predict_all, kernel_launch_count, knn_stage, make_grid_config, raster_lattice, run_pipeline,
-    run_pipeline_device, set_alpha4_recipe, set_weight_precision)
+    Raster, RasterOutcome, RunConfig, aidw_predict_all, build_index, choose_cell_width,
+    compute_bbox, compute_bbox_device, device_info, generate_clustered, generate_random_points,
+    generate_random_queries, idw_predict_all, kernel_launch_count, knn_stage, make_grid_config,
+    raster_lattice, raster_lattice_device, run_pipeline, run_pipeline_device, run_raster,
+    set_alpha4_recipe, set_weight_precision, write_raster_asc)
 
 __version__ = "0.1.0"

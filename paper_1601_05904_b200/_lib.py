@@ -103,6 +103,14 @@ SIGNATURES = {
     "aidw_generate_clustered": (C.c_int, [C.c_size_t, C.c_int32, C.c_double, C.c_uint64,
                                           C.c_uint64, _dp, _dp, _dp, _ep]),
     "aidw_raster_lattice": (C.c_int, [C.c_size_t, C.c_size_t, _dp, _dp, _dp, _ep]),
+    "aidw_raster_lattice_device": (C.c_int, [C.c_size_t, C.c_size_t, _dp, C.c_size_t,
+                                             C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             _ep]),
+    "aidw_run_raster": (C.c_int, [_dp, _dp, _dp, C.c_size_t, C.c_size_t, C.c_size_t,
+                                  C.POINTER(RunConfig), _dp, _dp, _dp, C.POINTER(RunStats),
+                                  _ep]),
+    "aidw_write_raster_asc": (C.c_int, [C.c_char_p, C.c_size_t, C.c_size_t, C.c_double,
+                                        C.c_double, C.c_double, _dp, _ep]),
 }
 
 _lib = None

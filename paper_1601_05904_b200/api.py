@@ -399,6 +399,72 @@ def run_pipeline_device(d_dx, d_dy, d_dz, m, d_qx, d_qy, n, cfg: RunConfig, d_pr
     return st.as_dict()
 
 
+@dataclass
+class Raster:
+    """io.hpp:190-197: ncols x nrows values, northernmost row first."""
+    ncols: int
+    nrows: int
+    xllcorner: float
+    yllcorner: float
+    cellsize: float
+    values: np.ndarray  # (nrows * ncols,), row-major
+
+    def grid(self) -> np.ndarray:
+        return self.values.reshape(self.nrows, self.ncols)
+
+
+@dataclass
+class RasterOutcome:
+    """cli.hpp:476-480: the raster plus the underlying pipeline run."""
+    raster: Raster
+    pipeline: PipelineOutcome
+
+
+def run_raster(data: PointSet, nx: int, ny: int, cfg: RunConfig,
+               with_alpha: bool = True) -> RasterOutcome:
+    """The compute part of cli::cmd_raster (cli.hpp:484-524): the nx x ny
+    lattice over bbox(data) is generated in HBM (no host lattice, no query
+    upload), then the fused pipeline runs; host data in, raster out."""
+    if nx < 1 or ny < 1:
+        raise InvalidArgument("cmd_raster: nx and ny must be >= 1")
+    if data.count() == 0:
+        raise InvalidArgument("cmd_raster: data set is empty")
+    n = nx * ny
+    vals, alph, bb = np.empty(n), (np.empty(n) if with_alpha else None), np.empty(4)
+    st = L.RunStats()
+    c = cfg.c()
+    err = L.Error()
+    zs = data.zs if data.has_values() else None
+    _raise(lib().aidw_run_raster(_p(data.xs), _p(data.ys), _p(zs) if zs is not None else None,
+                                 data.count(), nx, ny, C.byref(c), _p(vals),
+                                 _p(alph) if with_alpha else None, _p(bb),
+                                 C.byref(st), C.byref(err)), err)
+    raster = Raster(nx, ny, float(bb[0]), float(bb[1]), (bb[2] - bb[0]) / nx, vals)
+    return RasterOutcome(raster, PipelineOutcome(InterpolationResult(vals, alph), st.as_dict(),
+                                                 int(st.k_effective)))
+
+
+def raster_lattice_device(nx, ny, bbox, d_xs, d_ys, row0=0, rows=None, stream=None):
+    """cmd_raster lattice rows [row0, row0 + rows) generated into device
+    buffers (raw pointers), cli.hpp:496-507."""
+    rows = ny - row0 if rows is None else rows
+    bb = _f64(bbox)
+    err = L.Error()
+    _raise(lib().aidw_raster_lattice_device(nx, ny, _p(bb), row0, rows, d_xs, d_ys, stream,
+                                            C.byref(err)), err)
+
+
+def write_raster_asc(path: str, raster: Raster) -> None:
+    """io.hpp:199-221, byte-identical output, parallel formatting."""
+    if len(raster.values) != raster.ncols * raster.nrows:
+        raise InvalidArgument("write_raster_asc: value count does not match dimensions")
+    v = _f64(raster.values)
+    err = L.Error()
+    _raise(lib().aidw_write_raster_asc(path.encode(), raster.ncols, raster.nrows,
+                                       float(raster.xllcorner), float(raster.yllcorner),
+                                       float(raster.cellsize), _p(v), C.byref(err)), err)
+
+
 def compute_bbox_device(d_dx, d_dy, m, d_qx, d_qy, n, stream=None):
     out = np.empty(4)
     err = L.Error()

@@ -569,6 +569,31 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
                       fails.h[kFailAlpha]);
 }
 
+// cmd_raster's query lattice (cli.hpp:496-507) generated in HBM: row-major,
+// northernmost row first, rows [row0, row0 + rows) of the ny-row lattice.
+// Explicit round-to-nearest ops keep the reference's two-rounding form.
+__global__ void lattice_kernel(size_t nx, size_t ny, double min_x, double min_y, double sx,
+                               double sy, size_t row0, size_t rows, double* __restrict__ qx,
+                               double* __restrict__ qy) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nx * rows) return;
+    const size_t r = row0 + i / nx, c = i % nx;
+    qx[i] = __dadd_rn(min_x, __dmul_rn(__dadd_rn(static_cast<double>(c), 0.5), sx));
+    qy[i] = __dadd_rn(min_y, __dmul_rn(__dadd_rn(static_cast<double>(ny - 1 - r), 0.5), sy));
+}
+
+void lattice_device(size_t nx, size_t ny, const double* bbox, size_t row0, size_t rows,
+                    double* d_qx, double* d_qy, cudaStream_t s) {
+    if (nx < 1 || ny < 1)
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "cmd_raster: nx and ny must be >= 1");
+    if (row0 + rows > ny) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "cmd_raster: row range outside the lattice");
+    const double sx = (bbox[2] - bbox[0]) / static_cast<double>(nx);  // cli.hpp:496-497
+    const double sy = (bbox[3] - bbox[1]) / static_cast<double>(ny);
+    if (nx * rows)
+        LAUNCH(lattice_kernel, ceil_div(nx * rows, kThreads), kThreads, 0, s, nx, ny, bbox[0],
+               bbox[1], sx, sy, row0, rows, d_qx, d_qy);
+}
+
 void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_stats* st,
                     cudaStream_t s, double h2d_ms, const std::chrono::steady_clock::time_point& t0,
                     double* h_pred, double* h_alpha) {
@@ -896,6 +921,50 @@ int aidw_run_pipeline_device(const double* d_dx, const double* d_dy, const doubl
         StreamScope ss(stream);
         PipelineIO io{d_dx, d_dy, d_dz, d_qx, d_qy, m, n, d_pred, d_alpha};
         pipeline_entry(io, *cfg, stats, ss.s, 0.0, t0, nullptr, nullptr);
+    });
+}
+
+int aidw_raster_lattice_device(size_t nx, size_t ny, const double* bbox, size_t row0,
+                               size_t rows, double* d_xs, double* d_ys, void* stream,
+                               aidw_error* err) {
+    return guarded(err, [&] {
+        StreamScope ss(stream);
+        lattice_device(nx, ny, bbox, row0, rows, d_xs, d_ys, ss.s);
+        ss.sync();
+    });
+}
+
+int aidw_run_raster(const double* dx, const double* dy, const double* dz, size_t m, size_t nx,
+                    size_t ny, const aidw_run_config* cfg, double* raster_out, double* alpha_out,
+                    double* bbox_out, aidw_run_stats* stats, aidw_error* err) {
+    return guarded(err, [&] {
+        if (!cfg) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "run_pipeline: config missing");
+        if (nx < 1 || ny < 1)
+            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "cmd_raster: nx and ny must be >= 1");
+        if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "cmd_raster: data set is empty");
+        const auto t0 = std::chrono::steady_clock::now();
+        StreamScope ss;
+        cudaStream_t s = ss.s;
+        const size_t n = nx * ny;
+        DBuf<double> ddx, ddy, ddz, dqx(n, s), dqy(n, s), pred(n, s), alpha(n, s);
+        h2d(ddx, dx, m, s);
+        h2d(ddy, dy, m, s);
+        if (dz) h2d(ddz, dz, m, s);
+        ss.sync();
+        const double h2d_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        // the lattice spans bbox(data) (cli.hpp:495); its cell centres lie
+        // inside it, so bbox(data ∪ lattice) is the same box
+        const Extents e = extents(ddx.get(), ddy.get(), m, nullptr, nullptr, 0, nullptr, 0, s);
+        const double bb[4] = {e.box.min_x, e.box.min_y, e.box.max_x, e.box.max_y};
+        if (bbox_out) std::memcpy(bbox_out, bb, sizeof bb);
+        lattice_device(nx, ny, bb, 0, ny, dqx.get(), dqy.get(), s);
+        aidw_run_config c = *cfg;
+        c.use_bbox = 1;
+        std::memcpy(c.bbox, bb, sizeof bb);
+        PipelineIO io{ddx.get(), ddy.get(), dz ? ddz.get() : nullptr, dqx.get(), dqy.get(), m, n,
+                      pred.get(), alpha.get()};
+        pipeline_entry(io, c, stats, s, h2d_ms, t0, raster_out, alpha_out);
     });
 }
 
