@@ -206,11 +206,47 @@ int aidw_run_raster(const double* dx, const double* dy, const double* dz, size_t
                     size_t ny, const aidw_run_config* cfg, double* raster_out, double* alpha_out,
                     double* bbox_out, aidw_run_stats* stats, aidw_error* err);
 
+/* ------------------------------------------------------------ files (io.hpp) */
+/* The file formats either side of the path, same bytes and diagnostics as
+ * proj/include/aidw/io.hpp, parsed / formatted on all host threads.
+ * Parse and I/O failures -> AIDW_ERR_RUNTIME with the reference's
+ * "<path>:<line>: ..." message; non-finite values -> AIDW_ERR_INVALID_ARGUMENT
+ * (validate_finite, types.hpp:146-159). */
+typedef struct aidw_points_buffer {
+    double* xs;
+    double* ys;
+    double* zs; /* NULL for query files */
+    size_t count;
+} aidw_points_buffer;
+
+/* read_data_csv (with_values = 1, header "x,y,z") / read_query_csv
+ * (with_values = 0, header "x,y") — io.hpp:103-145.  The library allocates
+ * the arrays; release them with aidw_free_points. */
+int aidw_read_points_csv(const char* path, int32_t with_values, aidw_points_buffer* out,
+                         aidw_error* err);
+void aidw_free_points(aidw_points_buffer* buf);
+
+/* write_data_csv / write_query_csv / write_result_csv (io.hpp:146-188):
+ * `header` then `rows` lines of ncols "%.17g" fields; cols[c][r]. */
+int aidw_write_columns_csv(const char* path, const char* header, size_t rows, int32_t ncols,
+                           const double* const* cols, aidw_error* err);
+
 /* write_raster_asc (io.hpp:199-221): the ESRI ASCII grid, byte-identical to
- * the reference writer ("%.17g" values), formatted on all host threads. */
+ * the reference writer ("%.17g" values). */
 int aidw_write_raster_asc(const char* path, size_t ncols, size_t nrows, double xllcorner,
                           double yllcorner, double cellsize, const double* values,
                           aidw_error* err);
+
+typedef struct aidw_raster_buffer {
+    size_t ncols, nrows;
+    double xllcorner, yllcorner, cellsize;
+    double* values; /* nrows * ncols, north-first; free with aidw_free_raster */
+    size_t count;
+} aidw_raster_buffer;
+
+/* parse_raster_asc (io.hpp:223-253). */
+int aidw_read_raster_asc(const char* path, aidw_raster_buffer* out, aidw_error* err);
+void aidw_free_raster(aidw_raster_buffer* buf);
 
 /* ------------------------------------------------------------ synthetic inputs */
 /* generate_random_points / generate_random_queries — generate.hpp:45-95

@@ -407,3 +407,18 @@ def ref_cmd_raster(dx, dy, dz, nx, ny, k=15, workers=0, tmpdir="/tmp"):
            m.value)
     return vals, dict(zip(("ncols", "nrows", "xllcorner", "yllcorner", "cellsize"), meta)), \
         asc.decode()
+
+
+def ref_read_points_csv(path, with_values=True, cap=1 << 22):
+    """The reference's read_data_csv / read_query_csv.  Returns (xs, ys, zs)
+    or raises OracleError(code, message)."""
+    xs, ys, zs = np.empty(cap), np.empty(cap), np.empty(cap)
+    count = C.c_size_t()
+    m = _msg()
+    rc = ref().ref_read_points_csv(path.encode(), C.c_int(1 if with_values else 0),
+                                   C.c_size_t(cap), _p(xs, _dp), _p(ys, _dp), _p(zs, _dp),
+                                   C.byref(count), m, C.c_size_t(_MSG))
+    if rc != 0:
+        raise OracleError(rc, m.value.decode(), -1)
+    n = count.value
+    return xs[:n].copy(), ys[:n].copy(), (zs[:n].copy() if with_values else None)

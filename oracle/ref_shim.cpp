@@ -298,6 +298,22 @@ int ref_cmd_raster(const double* dx, const double* dy, const double* dz, std::si
     }
 }
 
+// read_data_csv / read_query_csv (io.hpp:103-145): up to `cap` points.
+int ref_read_points_csv(const char* path, int with_values, std::size_t cap, double* xs,
+                        double* ys, double* zs, std::size_t* count, char* msg, std::size_t mcap) {
+    try {
+        const aidw::PointSet set = with_values ? aidw::read_data_csv(path) : aidw::read_query_csv(path);
+        *count = set.count();
+        const std::size_t n = set.count() < cap ? set.count() : cap;
+        std::memcpy(xs, set.xs.data(), n * sizeof(double));
+        std::memcpy(ys, set.ys.data(), n * sizeof(double));
+        if (with_values) std::memcpy(zs, set.zs.data(), n * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return classify(e, msg, mcap);
+    }
+}
+
 int ref_hardware_threads() { return aidw::resolve_workers(0); }
 
 }  // extern "C"

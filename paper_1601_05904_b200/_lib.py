@@ -71,6 +71,17 @@ _i64p = C.POINTER(C.c_int64)
 _u8p = C.POINTER(C.c_uint8)
 _ep = C.POINTER(Error)
 
+class PointsBuffer(C.Structure):
+    _fields_ = [("xs", C.POINTER(C.c_double)), ("ys", C.POINTER(C.c_double)),
+                ("zs", C.POINTER(C.c_double)), ("count", C.c_size_t)]
+
+
+class RasterBuffer(C.Structure):
+    _fields_ = [("ncols", C.c_size_t), ("nrows", C.c_size_t), ("xllcorner", C.c_double),
+                ("yllcorner", C.c_double), ("cellsize", C.c_double),
+                ("values", C.POINTER(C.c_double)), ("count", C.c_size_t)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/aidw_capi.h
 SIGNATURES = {
     "aidw_capi_version": (C.c_int, []),
@@ -111,6 +122,12 @@ SIGNATURES = {
                                   _ep]),
     "aidw_write_raster_asc": (C.c_int, [C.c_char_p, C.c_size_t, C.c_size_t, C.c_double,
                                         C.c_double, C.c_double, _dp, _ep]),
+    "aidw_read_points_csv": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(PointsBuffer), _ep]),
+    "aidw_free_points": (None, [C.POINTER(PointsBuffer)]),
+    "aidw_write_columns_csv": (C.c_int, [C.c_char_p, C.c_char_p, C.c_size_t, C.c_int32,
+                                         C.POINTER(_dp), _ep]),
+    "aidw_read_raster_asc": (C.c_int, [C.c_char_p, C.POINTER(RasterBuffer), _ep]),
+    "aidw_free_raster": (None, [C.POINTER(RasterBuffer)]),
 }
 
 _lib = None

@@ -465,6 +465,75 @@ def write_raster_asc(path: str, raster: Raster) -> None:
                                        float(raster.cellsize), _p(v), C.byref(err)), err)
 
 
+# ------------------------------------------------------------ files (io.hpp)
+def _read_points(path, with_values):
+    buf = L.PointsBuffer()
+    err = L.Error()
+    _raise(lib().aidw_read_points_csv(path.encode(), 1 if with_values else 0, C.byref(buf),
+                                      C.byref(err)), err)
+    try:
+        n = buf.count
+        xs = np.ctypeslib.as_array(buf.xs, (n,)).copy() if n else np.empty(0)
+        ys = np.ctypeslib.as_array(buf.ys, (n,)).copy() if n else np.empty(0)
+        zs = (np.ctypeslib.as_array(buf.zs, (n,)).copy() if n else np.empty(0)) \
+            if with_values else np.empty(0)
+    finally:
+        lib().aidw_free_points(C.byref(buf))
+    return PointSet(xs, ys, zs)
+
+
+def read_data_csv(path: str) -> PointSet:
+    """io.hpp:103-124: header `x,y,z`; parallel parse, reference diagnostics."""
+    return _read_points(path, True)
+
+
+def read_query_csv(path: str) -> PointSet:
+    """io.hpp:126-145: header `x,y`."""
+    return _read_points(path, False)
+
+
+def _write_columns(path, header, cols):
+    cols = [_f64(c) for c in cols]
+    arr = (L._dp * len(cols))(*[_p(c) for c in cols])
+    err = L.Error()
+    _raise(lib().aidw_write_columns_csv(path.encode(), header.encode(), len(cols[0]), len(cols),
+                                        arr, C.byref(err)), err)
+
+
+def write_data_csv(path: str, data: PointSet) -> None:
+    """io.hpp:146-156 ("%.17g" fields, byte-identical)."""
+    if not data.has_values():
+        raise InvalidArgument("write_data_csv: point set carries no values")
+    _write_columns(path, "x,y,z", [data.xs, data.ys, data.zs])
+
+
+def write_query_csv(path: str, queries: PointSet) -> None:
+    """io.hpp:158-167."""
+    _write_columns(path, "x,y", [queries.xs, queries.ys])
+
+
+def write_result_csv(path: str, queries: PointSet, result: InterpolationResult) -> None:
+    """io.hpp:169-188: `x,y,alpha,z_pred`, input order."""
+    n = queries.count()
+    if len(result.predicted) != n or len(result.alphas) != n:
+        raise InvalidArgument("write_result_csv: result length does not match queries")
+    _write_columns(path, "x,y,alpha,z_pred", [queries.xs, queries.ys, result.alphas,
+                                              result.predicted])
+
+
+def parse_raster_asc(path: str) -> Raster:
+    """io.hpp:223-253."""
+    buf = L.RasterBuffer()
+    err = L.Error()
+    _raise(lib().aidw_read_raster_asc(path.encode(), C.byref(buf), C.byref(err)), err)
+    try:
+        vals = np.ctypeslib.as_array(buf.values, (buf.count,)).copy() if buf.count else np.empty(0)
+        return Raster(int(buf.ncols), int(buf.nrows), buf.xllcorner, buf.yllcorner, buf.cellsize,
+                      vals)
+    finally:
+        lib().aidw_free_raster(C.byref(buf))
+
+
 def compute_bbox_device(d_dx, d_dy, m, d_qx, d_qy, n, stream=None):
     out = np.empty(4)
     err = L.Error()

@@ -616,8 +616,10 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
     CK(cudaStreamSynchronize(s));
     if (st) {
         *st = local;
-        st->build_ms = Events::ms(marks[0], marks[1]);
-        st->knn_ms = Events::ms(marks[1], marks[2]);
+        // idw mode has no build / kNN stage (cli.hpp:227-234): exactly 0 ms
+        const bool idw = cfg.mode == AIDW_MODE_IDW;
+        st->build_ms = idw ? 0.0 : Events::ms(marks[0], marks[1]);
+        st->knn_ms = idw ? 0.0 : Events::ms(marks[1], marks[2]);
         st->interp_ms = Events::ms(marks[2], marks[3]);
         st->weight_kernel_ms = Events::ms(k4b, k4e);
         st->knn_kernel_ms = Events::ms(knnb, knne);

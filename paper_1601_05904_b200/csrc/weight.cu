@@ -173,8 +173,12 @@ __global__ void tile_geo_kernel(float* __restrict__ rec, size_t m, size_t tiles,
     const float cx = 0.5f * (x0 + x1), cy = 0.5f * (y0 + y1);
     const float gx = x1 - x0, gy = y1 - y0;
     const bool partial = (tile + 1) * kWeightTile > m;
+#if AIDW_K4_EXPERIMENT_ALLFAR  // timing experiment only: every full tile far
+    const float thr2 = partial ? INFINITY : 1.0e-8f;
+#else
     const float thr2 =
         partial ? INFINITY : fmaxf(fmaxf(rfar2, 1.0e-8f), 1.001f * diagf2 * fmaf(gx, gx, gy * gy));
+#endif
     if (lane == 0) {
         box[tile] = make_float4(x0, y0, x1, y1);
         geo[tile] = make_float4(cx, cy, thr2, 0.0f);

@@ -1,4 +1,6 @@
-"""Drop-in conformance: the reference's OWN test sources, compiled unchanged
+"""Drop-in conformance: the reference's OWN test sources (all of them: the
+acceptance gate and the eight Catch2 suites, including test_io / test_cli
+for the file formats and commands either side of the path), compiled unchanged
 against include/aidw + libaidw_b200.so (oracle/Makefile target
 `conformance`, built by __graft_entry__.build() where /root/reference is
 mounted; the binaries travel to the GPU box in oracle/_ref/conformance/).
@@ -41,7 +43,8 @@ def test_reference_host_suites(suite):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["test_grid", "test_knn", "test_interpolate", "test_core"])
+@pytest.mark.parametrize("suite", ["test_grid", "test_knn", "test_interpolate", "test_core",
+                                   "test_io", "test_cli"])
 def test_reference_gpu_suites_fp64(suite):
     rc, out = run(suite, {"AIDW_WEIGHT_FP64": "1"})
     assert rc == 0, out
@@ -54,7 +57,8 @@ FP32_ALLOWED = {
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["test_grid", "test_knn", "test_interpolate"])
+@pytest.mark.parametrize("suite", ["test_grid", "test_knn", "test_interpolate", "test_io",
+                                   "test_cli"])
 def test_reference_gpu_suites_fp32(suite):
     rc, out = run(suite)
     bad = failed_cases(out) - FP32_ALLOWED.get(suite, set())
