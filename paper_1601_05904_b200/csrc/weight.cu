@@ -30,6 +30,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -245,8 +246,10 @@ __global__ void morton_keys_kernel(const WeightQueries q, WeightFrame f, uint32_
     if (p >= q.n) return;
     const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
     const double xn = (q.qx[qi] - f.ox) * f.inv_scale, yn = (q.qy[qi] - f.oy) * f.inv_scale;
-    const uint32_t cx = static_cast<uint32_t>(fmin(fmax(xn * 65536.0, 0.0), 65535.0));
-    const uint32_t cy = static_cast<uint32_t>(fmin(fmax(yn * 65536.0, 0.0), 65535.0));
+    // 256 x 256 Morton cells: fine enough for warp / CTA locality, and a
+    // 16-bit key sorts in two radix passes
+    const uint32_t cx = static_cast<uint32_t>(fmin(fmax(xn * 256.0, 0.0), 255.0));
+    const uint32_t cy = static_cast<uint32_t>(fmin(fmax(yn * 256.0, 0.0), 255.0));
     key[p] = spread16(cx) | (spread16(cy) << 1);
     pos[p] = static_cast<uint32_t>(p);
 }
@@ -863,10 +866,17 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
 void set_alpha4_recipe(bool enabled) { g_alpha4_recipe.store(enabled); }
 
 WeightSplit weight_split(size_t m) {
+    // Data chunks per query (the grid's y dimension): enough CTAs to fill
+    // 148 SMs at small n without a partial last wave dominating — up to 64
+    // chunks of >= 8 tiles while m <= 256K, 16 chunks beyond (partials stay
+    // 256 B per query).  A function of m only, so a query's summation order
+    // never depends on n, the shard or the GPU count.
     WeightSplit w;
     w.tiles = (m + kWeightTile - 1) / kWeightTile;
     if (w.tiles == 0) w.tiles = 1;
-    size_t chunks = w.tiles < static_cast<size_t>(kMaxChunks) ? w.tiles : kMaxChunks;
+    const size_t cap = w.tiles <= 1024 ? 64 : static_cast<size_t>(kMaxChunks);
+    size_t chunks = std::min(cap, std::max<size_t>(1, w.tiles / 8));
+    if (w.tiles > 1024) chunks = std::min(w.tiles, static_cast<size_t>(kMaxChunks));
     w.tiles_per_chunk = (w.tiles + chunks - 1) / chunks;
     w.chunks = static_cast<unsigned>((w.tiles + w.tiles_per_chunk - 1) / w.tiles_per_chunk);
     return w;
@@ -910,7 +920,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     DBuf<uint32_t> zkey(q.n, s), zpos(q.n, s);
     LAUNCH(morton_keys_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, zkey.get(),
            zpos.get());
-    radix_sort_pairs(zkey.get(), zpos.get(), q.n, 32, s);
+    radix_sort_pairs(zkey.get(), zpos.get(), q.n, 16, s);
     zkey.release();
     // share of general-alpha queries on the FMA-pipe exp2 (G2); the rest of
     // a G1 / G2 interleave runs as all-G2 warps (AIDW_K4_G2 to tune)
