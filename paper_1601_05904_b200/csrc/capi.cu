@@ -336,15 +336,8 @@ void weighting_stage(const double* d_dx, const double* d_dy, const double* d_dz,
                      FailFlags& fails, WeightTimes* wt, cudaStream_t s) {
     const WeightFrame frame = make_frame(ext.box, ext.zlo, ext.zhi);
     WeightData wd{d_dx, d_dy, d_dz, m};
-    if (mode != WeightMode::fp32) {
-        WeightQueries q;
-        q.qx = d_qx;
-        q.qy = d_qy;
-        q.n = n;
-        q.alpha_s = d_alpha_q;
-        weighting_fp64(q, wd, frame, mode == WeightMode::fp64_blocked, d_pred, d_alpha_out, wt, s);
-        return;
-    }
+    // snap index, nearest index and d2_min per query (k = 1 grid search,
+    // FP64): the weighting kernels' snap rule and non-finite fallback
     NearestInfo nb;
     nearest_search(d_dx, d_dy, m, d_qx, d_qy, n, ext.box, frame.snap_sq, nb, fails, s);
     const uint32_t* perm = nb.perm.n ? nb.perm.get() : nullptr;
@@ -361,7 +354,10 @@ void weighting_stage(const double* d_dx, const double* d_dy, const double* d_dz,
     q.d2min_s = nb.d2min.get();
     q.nn_s = nb.nn.get();
     q.snap_s = nb.snap.get();
-    weighting_fp32(q, wd, frame, d_pred, d_alpha_out, wt, s);
+    if (mode != WeightMode::fp32)
+        weighting_fp64(q, wd, frame, mode == WeightMode::fp64_blocked, d_pred, d_alpha_out, wt, s);
+    else
+        weighting_fp32(q, wd, frame, d_pred, d_alpha_out, wt, s);
 }
 
 void fill_error(aidw_error* err, int code, const std::string& msg, long long index) {

@@ -8,9 +8,10 @@
 //          half-integer recipe d2^(n/4) via products and square roots when
 //          2a is an integer in [1, 16], else exp(-a/2 log d2); 256-point
 //          chunk partial sums folded into running sums.
-// Both: one thread per query, data streamed through shared memory in index
-// order, snap on the first index with d2 <= snap_sq, non-finite sums ->
-// nearest value (strict <, lowest index), clamp to the value hull.
+// Both: four queries per thread, data streamed through shared memory in
+// index order; snap on the first index with d2 <= snap_sq and the non-finite
+// fallback to the nearest value (strict <, lowest index) use the indices of
+// the k = 1 grid search; clamp to the value hull.
 // Compiled with -fmad=false and explicit _rn intrinsics: roundings match
 // the reference except CUDA's pow / exp / log (<= 2 ulp vs glibc; contract
 // 2e-11 relative).
@@ -42,85 +43,157 @@ __device__ __forceinline__ double recipe_denominator(double d2, int n4) {
     return den;
 }
 
-template <bool BLOCKED>
+// One thread carries QT queries (visiting positions p, p + 128, ...), so a
+// broadcast shared-memory read of one data point feeds QT pairs; the data
+// stream through shared memory in index order, 256-point tiles.  The snap
+// index and the nearest index come from the k = 1 grid search (FP64, the
+// same d2 as here: identical first-index / lowest-index semantics), so the
+// inner loop is branch-free FP64 arithmetic: d2, the weight, the sums.
+__device__ __forceinline__ bool recipe_alpha(double alpha) {
+    const double twice = 2.0 * alpha;
+    return twice == floor(twice) && twice >= 1.0 && twice <= 16.0;
+}
+
+// Slots ordered alpha == 4 first, then the other recipe alphas, then
+// exp / log (BLOCKED), so a warp's queries share one weight formula (a single
+// exp/log query would otherwise put its whole warp on the exp/log path, and
+// alpha == 4 warps take a specialised loop).
+__global__ void fp64_class_kernel(const WeightQueries q, int blocked, uint32_t* __restrict__ flag) {
+    const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < q.n) flag[p] = (blocked && q.alpha_s[p] != 4.0) ? 1u : 0u;
+}
+
+// 1 / x to ~1 ulp on the FP64 pipe: MUFU.RCP64H seed + two Newton steps,
+// branch-free (x here is a positive normal d2^2).  The FP64 blocked
+// kernel's contract is 2e-11 relative; its sums already differ in order from
+// the reference's SIMD lanes.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(r, fma(-x, r, 1.0), r);
+    return fma(r, fma(-x, r, 1.0), r);
+}
+
+__global__ void fp64_order_kernel(const uint32_t* __restrict__ flag,
+                                  const uint32_t* __restrict__ scan, size_t n,
+                                  uint32_t* __restrict__ order) {
+    const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const size_t general = static_cast<size_t>(scan[n - 1]) + flag[n - 1];
+    const size_t slot = flag[p] ? (n - general) + scan[p] : p - scan[p];
+    order[slot] = static_cast<uint32_t>(p);
+}
+
+template <bool BLOCKED, int QT>
 __global__ void __launch_bounds__(128) weight_fp64_kernel(const WeightQueries q,
                                                           const WeightFrame f,
                                                           const WeightData d,
+                                                          const uint32_t* __restrict__ order,
                                                           double* __restrict__ pred,
                                                           double* __restrict__ alpha_out) {
-    __shared__ double sx[kTile64], sy[kTile64], sz[kTile64];
-    const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool live = p < q.n;
-    uint32_t qi = 0;
-    double qx = 0.0, qy = 0.0, alpha = 1.0;
-    if (live) {
-        qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
-        qx = q.qx[qi];
-        qy = q.qy[qi];
-        alpha = q.alpha_s[p];
+    __shared__ double2 sxy[kTile64];
+    __shared__ double sz[kTile64];
+    const size_t p0 = static_cast<size_t>(blockIdx.x) * blockDim.x * QT + threadIdx.x;
+    double qx[QT], qy[QT], alpha[QT], e[QT], sw[QT], swz[QT];
+    int n4[QT];
+#pragma unroll
+    for (int i = 0; i < QT; ++i) {
+        const size_t slot = p0 + static_cast<size_t>(i) * blockDim.x;
+        const size_t p = slot < q.n ? order[slot] : slot;
+        qx[i] = qy[i] = 0.0;
+        alpha[i] = 4.0;
+        if (slot < q.n) {
+            const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
+            qx[i] = q.qx[qi];
+            qy[i] = q.qy[qi];
+            alpha[i] = q.alpha_s[p];
+        }
+        e[i] = -0.5 * alpha[i];
+        const double twice = 2.0 * alpha[i];
+        // the half-integer recipe (interpolate.hpp:174-192): 2a in [1, 16]
+        n4[i] = recipe_alpha(alpha[i]) ? static_cast<int>(twice) : 0;
+        sw[i] = swz[i] = 0.0;
     }
-    bool active = live;
-    double out = 0.0;
-    const double e = -0.5 * alpha;
-    const double twice = 2.0 * alpha;
-    const bool exact = twice == floor(twice) && twice >= 1.0 && twice <= 16.0;
-    const int n4 = exact ? static_cast<int>(twice) : 0;
-    double sw = 0.0, swz = 0.0;
-    double best = 0.0;
-    size_t best_i = 0;
+    bool four = true;
+#pragma unroll
+    for (int i = 0; i < QT; ++i) four &= alpha[i] == 4.0;
+    const bool all4 = __all_sync(0xFFFFFFFFu, four);
     for (size_t base = 0; base < d.m; base += kTile64) {
         const int len = static_cast<int>(d.m - base < kTile64 ? d.m - base : kTile64);
         __syncthreads();
         for (int j = threadIdx.x; j < len; j += blockDim.x) {
-            sx[j] = d.x[base + j];
-            sy[j] = d.y[base + j];
+            sxy[j] = make_double2(d.x[base + j], d.y[base + j]);
             sz[j] = d.z[base + j];
         }
         __syncthreads();
-        if (!active) continue;
-        double cw = 0.0, cwz = 0.0;  // chunk partials (BLOCKED)
+        double cw[QT], cwz[QT];  // chunk partials (BLOCKED)
+#pragma unroll
+        for (int i = 0; i < QT; ++i) cw[i] = cwz[i] = 0.0;
+        if (BLOCKED && all4) {  // warp-uniform alpha == 4: w = 1 / (d2 d2)
+            for (int j = 0; j < len; ++j) {
+                const double2 xy = sxy[j];
+                const double z = sz[j];
+#pragma unroll
+                for (int i = 0; i < QT; ++i) {
+                    const double d2 = dsq_rn(qx[i], qy[i], xy.x, xy.y);
+                    const double w = rcp_nr(__dmul_rn(d2, d2));
+                    cw[i] = __dadd_rn(cw[i], w);
+                    cwz[i] = __dadd_rn(cwz[i], __dmul_rn(w, z));
+                }
+            }
+        } else
         for (int j = 0; j < len; ++j) {
-            const double d2 = dsq_rn(qx, qy, sx[j], sy[j]);
-            if (d2 <= f.snap_sq) {
-                out = sz[j];
-                active = false;
-                break;
-            }
-            if ((base == 0 && j == 0) || d2 < best) {
-                best = d2;
-                best_i = base + j;
-            }
-            if (BLOCKED) {
-                const double w = exact ? __ddiv_rn(1.0, recipe_denominator(d2, n4))
-                                       : exp(__dmul_rn(e, log(d2)));
-                cw = __dadd_rn(cw, w);
-                cwz = __dadd_rn(cwz, __dmul_rn(w, sz[j]));
-            } else {
-                const double w = __ddiv_rn(1.0, pow(__dsqrt_rn(d2), alpha));
-                sw = __dadd_rn(sw, w);
-                swz = __dadd_rn(swz, __dmul_rn(w, sz[j]));
+            const double2 xy = sxy[j];
+            const double z = sz[j];
+#pragma unroll
+            for (int i = 0; i < QT; ++i) {
+                const double d2 = dsq_rn(qx[i], qy[i], xy.x, xy.y);
+                if (BLOCKED) {
+                    const double w = n4[i] ? __drcp_rn(recipe_denominator(d2, n4[i]))
+                                           : exp(__dmul_rn(e[i], log(d2)));
+                    cw[i] = __dadd_rn(cw[i], w);
+                    cwz[i] = __dadd_rn(cwz[i], __dmul_rn(w, z));
+                } else {
+                    const double w = __drcp_rn(pow(__dsqrt_rn(d2), alpha[i]));
+                    sw[i] = __dadd_rn(sw[i], w);
+                    swz[i] = __dadd_rn(swz[i], __dmul_rn(w, z));
+                }
             }
         }
-        if (BLOCKED && active) {
-            sw = __dadd_rn(sw, cw);
-            swz = __dadd_rn(swz, cwz);
+        if (BLOCKED) {
+#pragma unroll
+            for (int i = 0; i < QT; ++i) {
+                sw[i] = __dadd_rn(sw[i], cw[i]);
+                swz[i] = __dadd_rn(swz[i], cwz[i]);
+            }
         }
     }
-    if (!live) return;
-    if (active) {
-        // settle (interpolate.hpp:109-118)
-        bool ok = false;
-        if (sw > 0.0 && isfinite(sw) && isfinite(swz)) {
-            const double v = __ddiv_rn(swz, sw);
-            if (isfinite(v)) {
-                out = v < f.zlo ? f.zlo : (v > f.zhi ? f.zhi : v);
-                ok = true;
+#pragma unroll
+    for (int i = 0; i < QT; ++i) {
+        const size_t slot = p0 + static_cast<size_t>(i) * blockDim.x;
+        if (slot >= q.n) continue;
+        const size_t p = order[slot];
+        const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
+        double out;
+        const uint32_t snap = q.snap_s[p];
+        if (snap != kNoId) {
+            out = d.z[snap];  // first index within snap distance
+        } else {
+            // settle (interpolate.hpp:109-118)
+            bool ok = false;
+            out = 0.0;
+            if (sw[i] > 0.0 && isfinite(sw[i]) && isfinite(swz[i])) {
+                const double v = __ddiv_rn(swz[i], sw[i]);
+                if (isfinite(v)) {
+                    out = v < f.zlo ? f.zlo : (v > f.zhi ? f.zhi : v);
+                    ok = true;
+                }
             }
+            if (!ok) out = d.z[q.nn_s[p]];  // nearest_value: lowest index on ties
         }
-        if (!ok) out = d.z[best_i];
+        pred[qi] = out;
+        if (alpha_out) alpha_out[qi] = alpha[i];
     }
-    pred[qi] = out;
-    if (alpha_out) alpha_out[qi] = alpha;
 }
 
 }  // namespace
@@ -129,11 +202,31 @@ void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFra
                     bool blocked, double* d_pred, double* d_alpha, WeightTimes* times,
                     cudaStream_t s) {
     if (q.n == 0) return;
-    if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+    if (!q.snap_s || !q.nn_s)
+        throw Failure(AIDW_ERR_RUNTIME, "weighting_fp64: nearest / snap indices missing");
+    // queries per thread: 4 once that still leaves ~8 CTAs per SM, else
+    // fewer (the per-query arithmetic and order are the same for any QT)
+    const size_t per_sm = 8 * 148 * 128;
+    const int qt = q.n >= 4 * per_sm ? 4 : (q.n >= 2 * per_sm ? 2 : 1);
+    DBuf<uint32_t> flag(q.n, s), scan(q.n, s), order(q.n, s);
+    LAUNCH(fp64_class_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, blocked ? 1 : 0,
+           flag.get());
+    exclusive_scan_u32(flag.get(), scan.get(), q.n, s);
+    LAUNCH(fp64_order_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, flag.get(), scan.get(), q.n,
+           order.get());
+    auto go = [&](auto kernel, int k) {
+        if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+        LAUNCH(kernel, ceil_div(q.n, static_cast<size_t>(128 * k)), 128, 0, s, q, f, d,
+               order.get(), d_pred, d_alpha);
+    };
     if (blocked) {
-        LAUNCH(weight_fp64_kernel<true>, ceil_div(q.n, 128), 128, 0, s, q, f, d, d_pred, d_alpha);
+        if (qt == 4) go(weight_fp64_kernel<true, 4>, 4);
+        else if (qt == 2) go(weight_fp64_kernel<true, 2>, 2);
+        else go(weight_fp64_kernel<true, 1>, 1);
     } else {
-        LAUNCH(weight_fp64_kernel<false>, ceil_div(q.n, 128), 128, 0, s, q, f, d, d_pred, d_alpha);
+        if (qt == 4) go(weight_fp64_kernel<false, 4>, 4);
+        else if (qt == 2) go(weight_fp64_kernel<false, 2>, 2);
+        else go(weight_fp64_kernel<false, 1>, 1);
     }
     if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
 }
