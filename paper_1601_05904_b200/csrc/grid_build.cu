@@ -7,10 +7,12 @@
 //                         rounding), key = row-major cell id, value = index,
 //                         per-cell histogram with global atomics;
 //   2. exclusive_scan   : cell_start = exclusive prefix of the histogram;
-//   3. radix_sort_pairs : stable LSD radix sort (8-bit digits, warp-level
-//                         __match_any ranking) of (cell id, index) -> ids
-//                         grouped by cell, ascending index within a cell;
-//   4. gather_kernel    : cell-sorted copies of x / y.
+//   3. counting sort    : scatter through per-cell atomic cursors, then each
+//                         cell's ids sorted ascending (thread per cell of <= 16
+//                         points, warp rank placement up to 256, CTA bitonic up
+//                         to 4096, stable compaction beyond) fused with the gather of the cell-sorted
+//                         x / y.  (radix_sort_pairs — stable LSD, 8-bit digits,
+//                         warp __match_any ranking — sorts the queries by cell.)
 // All arrays are bit-identical to the reference's (tests/test_gpu_parity.py).
 // Compiled with -fmad=false: every FP64 expression keeps the reference's
 // two-rounding form.
@@ -51,22 +53,6 @@ __global__ void cell_ids_kernel(const double* __restrict__ x, const double* __re
     }
     keys[i] = cell;
     vals[i] = static_cast<uint32_t>(i);
-}
-
-__global__ void gather_kernel(const uint32_t* __restrict__ order, const double* __restrict__ x,
-                              const double* __restrict__ y, size_t m,
-                              uint32_t* __restrict__ ids, double2* __restrict__ sxy,
-                              double* __restrict__ sx, double* __restrict__ sy) {
-    const size_t s = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (s >= m) return;
-    const uint32_t id = order[s];
-    const double px = x[id], py = y[id];
-    ids[s] = id;
-    sxy[s] = make_double2(px, py);
-    if (sx) {
-        sx[s] = px;
-        sy[s] = py;
-    }
 }
 
 __global__ void interleave_kernel(const double* __restrict__ x, const double* __restrict__ y,
@@ -281,6 +267,161 @@ __global__ void decode_minmax_kernel(const unsigned long long* __restrict__ keys
     }
 }
 
+// ---------------------------------------------------------------- counting sort
+// The CSR arrays of build_index as a counting sort (grid.hpp:176-213 is one
+// too): histogram (cell_ids_kernel) -> exclusive scan (cell_start) ->
+// scatter through per-cell atomic cursors (order within a cell arbitrary) ->
+// each cell's ids sorted ascending, which is exactly the reference's stable
+// order, fused with the coordinate gather.  Cells of <= kSmallCell points
+// are sorted by one thread each, up to kMidCell by a warp, larger ones by a
+// CTA (cell_sort_big_kernel).
+constexpr int kSmallCell = 16;
+constexpr int kMidCell = 256;
+constexpr int kBigCell = 4096;
+
+__global__ void cell_scatter_kernel(const uint32_t* __restrict__ keys, size_t m,
+                                    uint32_t* __restrict__ cursor, uint32_t* __restrict__ ids) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < m) ids[atomicAdd(&cursor[keys[i]], 1u)] = static_cast<uint32_t>(i);
+}
+
+__device__ __forceinline__ void emit_point(size_t s, uint32_t id, const double* __restrict__ x,
+                                           const double* __restrict__ y, uint32_t* __restrict__ ids,
+                                           double2* __restrict__ sxy, double* __restrict__ sx,
+                                           double* __restrict__ sy) {
+    const double px = x[id], py = y[id];
+    ids[s] = id;
+    sxy[s] = make_double2(px, py);
+    if (sx) {
+        sx[s] = px;
+        sy[s] = py;
+    }
+}
+
+// One thread per cell of <= kSmallCell points: insertion sort in registers /
+// L1, then the gather.  Larger cells are queued for cell_sort_big_kernel.
+__global__ void cell_sort_small_kernel(const uint32_t* __restrict__ cell_start, size_t cells,
+                                       const uint32_t* __restrict__ scattered,
+                                       const double* __restrict__ x, const double* __restrict__ y,
+                                       uint32_t* __restrict__ ids, double2* __restrict__ sxy,
+                                       double* __restrict__ sx, double* __restrict__ sy,
+                                       uint32_t* __restrict__ mid, uint32_t* __restrict__ big,
+                                       uint32_t* __restrict__ nbig) {
+    const size_t c = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    const uint32_t b = cell_start[c], e = cell_start[c + 1];
+    const uint32_t n = e - b;
+    if (n == 0) return;
+    if (n > kSmallCell) {  // nbig[0]: warp-sized cells, nbig[1]: CTA-sized
+        if (n <= kMidCell) mid[atomicAdd(&nbig[0], 1u)] = static_cast<uint32_t>(c);
+        else big[atomicAdd(&nbig[1], 1u)] = static_cast<uint32_t>(c);
+        return;
+    }
+    uint32_t v[kSmallCell];
+    for (uint32_t j = 0; j < n; ++j) {
+        const uint32_t t = scattered[b + j];
+        uint32_t k = j;
+        while (k > 0 && v[k - 1] > t) {
+            v[k] = v[k - 1];
+            --k;
+        }
+        v[k] = t;
+    }
+    for (uint32_t j = 0; j < n; ++j) emit_point(b + j, v[j], x, y, ids, sxy, sx, sy);
+}
+
+// One warp per queued cell of kSmallCell < n <= kMidCell points: the ids go
+// to a per-warp shared buffer and each lane places its ids by rank (the
+// number of smaller ids in the cell; ids are distinct), then the gather.
+__global__ void __launch_bounds__(256) cell_sort_mid_kernel(
+    const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ mid,
+    const uint32_t* __restrict__ nmid, const uint32_t* __restrict__ scattered,
+    const double* __restrict__ x, const double* __restrict__ y, uint32_t* __restrict__ ids,
+    double2* __restrict__ sxy, double* __restrict__ sx, double* __restrict__ sy) {
+    __shared__ uint32_t buf[8][kMidCell];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + wp; w < *nmid; w += warps) {
+        const uint32_t c = mid[w];
+        const uint32_t b = cell_start[c], n = cell_start[c + 1] - b;
+        for (uint32_t j = lane; j < n; j += 32) buf[wp][j] = scattered[b + j];
+        __syncwarp();
+        for (uint32_t j = lane; j < n; j += 32) {
+            const uint32_t mine = buf[wp][j];
+            uint32_t rank = 0;
+            for (uint32_t k = 0; k < n; ++k) rank += buf[wp][k] < mine ? 1u : 0u;
+            emit_point(b + rank, mine, x, y, ids, sxy, sx, sy);
+        }
+        __syncwarp();
+    }
+}
+
+// One CTA per queued cell (n > kMidCell): a bitonic sort of the ids in
+// shared memory (padded with 0xFFFFFFFF) when n <= kBigCell, then the
+// gather.  A cell above kBigCell (degenerate, heavily duplicated data) is
+// instead rebuilt by a stable compaction of the key array in index order —
+// O(m) for that cell, correct for any size, no host round trip.
+__global__ void __launch_bounds__(256) cell_sort_big_kernel(
+    const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ big,
+    const uint32_t* __restrict__ nbig, const uint32_t* __restrict__ scattered,
+    const uint32_t* __restrict__ keys, size_t m, const double* __restrict__ x,
+    const double* __restrict__ y, uint32_t* __restrict__ ids, double2* __restrict__ sxy,
+    double* __restrict__ sx, double* __restrict__ sy) {
+    __shared__ uint32_t v[kBigCell];
+    __shared__ uint32_t wsum[8];
+    for (uint32_t w = blockIdx.x; w < *nbig; w += gridDim.x) {
+        const uint32_t c = big[w];
+        const uint32_t b = cell_start[c], n = cell_start[c + 1] - b;
+        __syncthreads();
+        if (n > static_cast<uint32_t>(kBigCell)) {
+            uint32_t run = 0;  // points of cell c before this chunk (all threads)
+            for (size_t base = 0; base < m; base += blockDim.x) {
+                const size_t i = base + threadIdx.x;
+                const bool hit = i < m && keys[i] == c;
+                const unsigned ball = __ballot_sync(0xFFFFFFFFu, hit);
+                const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+                if (lane == 0) wsum[wp] = __popc(ball);
+                __syncthreads();
+                uint32_t before = run, total = run;
+                for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) {
+                    if (k < wp) before += wsum[k];
+                    total += wsum[k];
+                }
+                if (hit) {
+                    const uint32_t s = b + before + __popc(ball & ((1u << lane) - 1u));
+                    emit_point(s, static_cast<uint32_t>(i), x, y, ids, sxy, sx, sy);
+                }
+                run = total;
+                __syncthreads();
+            }
+            continue;
+        }
+        uint32_t len = 1;
+        while (len < n) len <<= 1;
+        for (uint32_t j = threadIdx.x; j < len; j += blockDim.x)
+            v[j] = j < n ? scattered[b + j] : 0xFFFFFFFFu;
+        __syncthreads();
+        for (uint32_t size = 2; size <= len; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t j = threadIdx.x; j < len; j += blockDim.x) {
+                    const uint32_t partner = j ^ stride;
+                    if (partner > j) {
+                        const bool up = (j & size) == 0;
+                        const uint32_t a = v[j], o = v[partner];
+                        if ((a > o) == up) {
+                            v[j] = o;
+                            v[partner] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x)
+            emit_point(b + j, v[j], x, y, ids, sxy, sx, sy);
+    }
+}
+
 // Blocked cell order (K4 data tiles): cells visited in 8 x 8-cell blocks,
 // blocks row-major, cells row-major inside a block.  On a factor-4 grid a
 // block holds ~256 points (16 r_exp^2 m / A = 4 points per cell), so a
@@ -394,14 +535,28 @@ void build_grid_device(const double* d_x, const double* d_y, size_t m,
         out.sorted_x.alloc(m, s);
         out.sorted_y.alloc(m, s);
     }
-    DBuf<uint32_t> keys(m, s), vals(m, s);
+    DBuf<uint32_t> keys(m, s), vals(m, s), cursor(cells, s), mid(cells, s), big(cells, s),
+        nbig(2, s);
     CK(cudaMemsetAsync(out.cell_start.get(), 0, (cells + 1) * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(nbig.get(), 0, 2 * sizeof(uint32_t), s));
     LAUNCH(cell_ids_kernel, ceil_div(m, kThreads), kThreads, 0, s, d_x, d_y, m, g, keys.get(),
            vals.get(), out.cell_start.get(), d_fail);
     exclusive_scan_u32(out.cell_start.get(), out.cell_start.get(), cells + 1, s);
-    radix_sort_pairs(keys.get(), vals.get(), m, bits_for(cells - 1), s);
-    LAUNCH(gather_kernel, ceil_div(m, kThreads), kThreads, 0, s, vals.get(), d_x, d_y, m,
-           out.sorted_ids.get(), out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get());
+    // counting sort: cursors start at cell_start; vals receives the scatter
+    CK(cudaMemcpyAsync(cursor.get(), out.cell_start.get(), cells * sizeof(uint32_t),
+                       cudaMemcpyDeviceToDevice, s));
+    LAUNCH(cell_scatter_kernel, ceil_div(m, kThreads), kThreads, 0, s, keys.get(), m,
+           cursor.get(), vals.get());
+    LAUNCH(cell_sort_small_kernel, ceil_div(cells, kThreads), kThreads, 0, s,
+           out.cell_start.get(), cells, vals.get(), d_x, d_y, out.sorted_ids.get(),
+           out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get(), mid.get(), big.get(),
+           nbig.get());
+    LAUNCH(cell_sort_mid_kernel, 148u * 4u, 256, 0, s, out.cell_start.get(), mid.get(),
+           nbig.get(), vals.get(), d_x, d_y, out.sorted_ids.get(), out.sorted_xy.get(),
+           out.sorted_x.get(), out.sorted_y.get());
+    LAUNCH(cell_sort_big_kernel, 148u * 2u, 256, 0, s, out.cell_start.get(), big.get(),
+           nbig.get() + 1, vals.get(), keys.get(), m, d_x, d_y, out.sorted_ids.get(),
+           out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get());
 }
 
 void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, const GridGeom& g,

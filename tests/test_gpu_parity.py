@@ -76,6 +76,31 @@ def test_build_index_vs_oracle(m, factor, gen):
     assert np.array_equal(g.sorted_x, sx) and np.array_equal(g.sorted_y, sy)
 
 
+@pytest.mark.parametrize("dups,cells_wide", [(20, 4.0), (200, 4.0), (300, 4.0), (5000, 4.0), (9000, 64.0)])
+def test_build_index_crowded_cells(dups, cells_wide):
+    """Every per-cell sort path of the counting-sort build: thread per cell
+    (<= 16 points), CTA bitonic (17..4096), stable compaction (> 4096) —
+    duplicates of one point plus a jittered cluster, interleaved by index."""
+    rng = np.random.default_rng(dups)
+    bx, by, _ = O.generate_points(3000, UNIT, 5)
+    cx = np.full(dups, 0.5) + rng.integers(0, 3, dups) * 1e-9
+    cy = np.full(dups, 0.25)
+    xs = np.empty(3000 + dups)
+    ys = np.empty(3000 + dups)
+    order = rng.permutation(3000 + dups)
+    xs[order] = np.concatenate([bx, cx])
+    ys[order] = np.concatenate([by, cy])
+    bb = np.array(UNIT)
+    cfg_o = O.make_grid_config(bb, O.choose_cell_width(xs.size, bb, cells_wide))
+    ids, cs, sx, sy = O.build_index(xs, ys, cfg_o)
+    cfg = A.GridConfig(cfg_o.cell_width, cfg_o.n_col, cfg_o.n_row, cfg_o.min_x, cfg_o.min_y)
+    g = A.build_index(A.PointSet(xs, ys), cfg)
+    assert np.max(np.diff(cs)) >= dups
+    assert np.array_equal(g.sorted_point_ids, ids)
+    assert np.array_equal(g.cell_start, cs)
+    assert np.array_equal(g.sorted_x, sx) and np.array_equal(g.sorted_y, sy)
+
+
 def test_build_index_2x2_and_errors():  # test_grid.cpp:150-170, :276-279
     g = A.build_index(A.PointSet([1.5, 0.5, 1.5, 0.5], [0.5, 1.5, 1.5, 0.5]),
                       A.GridConfig(1.0, 2, 2, 0.0, 0.0))
