@@ -165,6 +165,17 @@ int aidw_idw_predict_all(const double* qx, const double* qy, size_t n, const dou
                          int32_t variant, int32_t pinned_order, double* pred_out,
                          double* alpha_out, aidw_error* err);
 
+/* ------------------------------------------------------------ devices */
+/* Devices aidw_run_pipeline / aidw_run_raster spread over (SURVEY §8e:
+ * one process, one host thread per device, query or lattice-row shards,
+ * data replicated, the global bbox combined before any grid is built ->
+ * results bit-identical to one device).  Default: the current device only,
+ * or AIDW_DEVICES="0,1,..." from the environment; a list may repeat a
+ * device.  count <= 1 restores the single-device default. */
+int aidw_set_devices(const int32_t* ids, int32_t count, aidw_error* err);
+/* Number of devices the pipeline calls use (>= 1). */
+int32_t aidw_device_count(void);
+
 /* ------------------------------------------------------------ pipeline */
 /* cli::run_pipeline — cli.hpp:217-268, fused and device-resident between
  * stages (no per-query KnnResult materialisation).  Host buffers. */

@@ -202,6 +202,20 @@ def set_alpha4_recipe(enabled: bool):
     lib().aidw_set_alpha4_recipe(1 if enabled else 0)
 
 
+def set_devices(ids) -> None:
+    """Devices run_pipeline / run_raster spread over, one host thread each
+    (query / lattice-row shards; results bit-identical to one device).
+    [] or a single id restores the single-device default."""
+    ids = list(ids)
+    arr = (C.c_int32 * max(1, len(ids)))(*ids)
+    err = L.Error()
+    _raise(lib().aidw_set_devices(arr, len(ids), C.byref(err)), err)
+
+
+def device_count() -> int:
+    return int(lib().aidw_device_count())
+
+
 def kernel_launch_count():
     return int(lib().aidw_kernel_launch_count())
 

@@ -19,7 +19,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <condition_variable>
+#include <functional>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <numbers>
 #include <string>
@@ -637,6 +641,293 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
     }
 }
 
+// ------------------------------------------------------------ multi-device
+// SURVEY §8e's single-process model: one host thread per device, the data
+// replicated to every device, a contiguous slice of the queries (or of the
+// raster's lattice rows) per device, and the global bbox(data ∪ all
+// queries) combined on the host before any grid is built — so every device
+// builds the identical grid, area and snap tolerance, and the result is
+// bit-identical to a one-device run (per-query formulas and summation order
+// depend on the query and m only).  Device list: aidw_set_devices or
+// AIDW_DEVICES="0,1,..."; a list may repeat a device (shards then share it).
+std::mutex g_dev_mu;
+std::vector<int> g_devices;
+bool g_dev_env_read = false;
+
+std::vector<int> device_list() {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_dev_env_read) {
+        g_dev_env_read = true;
+        if (const char* v = std::getenv("AIDW_DEVICES")) {
+            std::vector<int> ids;
+            const char* p = v;
+            while (*p) {
+                char* end = nullptr;
+                const long id = std::strtol(p, &end, 10);
+                if (end == p) break;
+                ids.push_back(static_cast<int>(id));
+                p = *end == ',' ? end + 1 : end;
+            }
+            if (g_devices.empty()) g_devices = ids;
+        }
+    }
+    return g_devices;
+}
+
+// One shard's device buffers (released on the shard's own thread).
+struct ShardBufs {
+    DBuf<double> dx, dy, dz, qx, qy, pred, alpha;
+    double h2d_ms = 0.0;
+    void release() {
+        dx.release(), dy.release(), dz.release(), qx.release(), qy.release();
+        pred.release(), alpha.release();
+    }
+};
+
+// A reusable-free count-down barrier for the shard threads.
+struct ShardBarrier {
+    std::mutex mu;
+    std::condition_variable cv;
+    size_t left;
+    explicit ShardBarrier(size_t n) : left(n) {}
+    void arrive_and_wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (--left == 0) {
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [this] { return left == 0; });
+        }
+    }
+};
+
+void shard_bounds(size_t n, size_t parts, size_t k, size_t& lo, size_t& hi) {
+    const size_t base = n / parts, extra = n % parts;
+    lo = k * base + std::min(k, extra);
+    hi = lo + base + (k < extra ? 1 : 0);
+}
+
+void merge_stats(aidw_run_stats& out, const aidw_run_stats* st, size_t count) {
+    out = st[0];
+    for (size_t d = 1; d < count; ++d) {
+        const aidw_run_stats& t = st[d];
+        out.build_ms = std::max(out.build_ms, t.build_ms);
+        out.knn_ms = std::max(out.knn_ms, t.knn_ms);
+        out.interp_ms = std::max(out.interp_ms, t.interp_ms);
+        out.total_ms = std::max(out.total_ms, t.total_ms);
+        out.weight_kernel_ms = std::max(out.weight_kernel_ms, t.weight_kernel_ms);
+        out.knn_kernel_ms = std::max(out.knn_kernel_ms, t.knn_kernel_ms);
+        out.h2d_ms = std::max(out.h2d_ms, t.h2d_ms);
+        out.d2h_ms = std::max(out.d2h_ms, t.d2h_ms);
+        out.pairs += t.pairs;
+        out.alpha4_queries += t.alpha4_queries;
+        out.knn_candidates += t.knn_candidates;
+        out.knn_ref_candidates += t.knn_ref_candidates;
+        out.kernel_launches += t.kernel_launches;
+    }
+}
+
+// One shard's work: `prep` uploads / generates its inputs on the shard's
+// device and returns its partial bbox; then (after all shards met) `run`
+// gets the global box.  Returns false if any shard failed (the caller then
+// re-runs on one device, which raises the reference's exact error).
+using ShardPrep = std::function<Box(size_t, cudaStream_t)>;
+using ShardRun = std::function<void(size_t, cudaStream_t, const Box&)>;
+using ShardFinish = std::function<void(size_t)>;
+
+void shard_thread(size_t d, int dev, const ShardPrep& prep, const ShardRun& run,
+                  const ShardFinish& finish, Box* boxes, char* failed, size_t D,
+                  ShardBarrier* sync) {
+    cudaStream_t s = nullptr;
+    try {
+        CK(cudaSetDevice(dev));
+        current_device();  // pool set-up for this device
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        boxes[d] = prep(d, s);
+    } catch (...) {
+        failed[d] = 1;
+    }
+    sync->arrive_and_wait();
+    bool any = false;
+    for (size_t k = 0; k < D; ++k) any |= failed[k] != 0;
+    if (!any) {
+        Box g = boxes[0];
+        for (size_t k = 1; k < D; ++k) {
+            g.min_x = std::min(g.min_x, boxes[k].min_x);
+            g.min_y = std::min(g.min_y, boxes[k].min_y);
+            g.max_x = std::max(g.max_x, boxes[k].max_x);
+            g.max_y = std::max(g.max_y, boxes[k].max_y);
+        }
+        try {
+            run(d, s, g);
+        } catch (...) {
+            failed[d] = 1;
+        }
+    }
+    try {
+        finish(d);  // buffers go back on this device / stream
+    } catch (...) {
+    }
+    if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+}
+
+// One shard's work: `prep` uploads / generates its inputs on the shard's
+// device and returns its partial bbox; then (after all shards met) `run`
+// gets the global box; `finish` releases its buffers.  Returns false if any
+// shard failed (the caller then re-runs on one device, which raises the
+// reference's exact error).
+bool run_sharded(const std::vector<int>& devs, const ShardPrep& prep, const ShardRun& run,
+                 const ShardFinish& finish) {
+    const size_t D = devs.size();
+    std::unique_ptr<Box[]> boxes(new Box[D]);
+    std::unique_ptr<char[]> failed(new char[D]());
+    ShardBarrier sync(D);
+    std::unique_ptr<std::thread[]> pool(new std::thread[D]);
+    for (size_t d = 0; d < D; ++d)
+        pool[d] = std::thread(shard_thread, d, devs[d], std::cref(prep), std::cref(run),
+                              std::cref(finish), boxes.get(), failed.get(), D, &sync);
+    for (size_t d = 0; d < D; ++d) pool[d].join();
+    for (size_t d = 0; d < D; ++d)
+        if (failed[d]) return false;
+    return true;
+}
+
+// run_pipeline over query shards, one per listed device.
+struct PipelineShards {
+    const double *dx, *dy, *dz, *qx, *qy;
+    size_t m, n, D;
+    aidw_run_config cfg;
+    double *pred_out, *alpha_out;
+    std::chrono::steady_clock::time_point t0;
+    ShardBufs* b;
+    aidw_run_stats* st;
+
+    Box prep(size_t d, cudaStream_t s) {
+        size_t lo, hi;
+        shard_bounds(n, D, d, lo, hi);
+        const auto c0 = std::chrono::steady_clock::now();
+        h2d(b[d].dx, dx, m, s);
+        h2d(b[d].dy, dy, m, s);
+        h2d(b[d].dz, dz, m, s);
+        h2d(b[d].qx, qx + lo, hi - lo, s);
+        h2d(b[d].qy, qy + lo, hi - lo, s);
+        b[d].pred.alloc(hi - lo, s);
+        b[d].alpha.alloc(hi - lo, s);
+        const Extents e =
+            extents(b[d].dx.get(), b[d].dy.get(), m, b[d].qx.get(), b[d].qy.get(), hi - lo, nullptr, 0, s);
+        b[d].h2d_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+        return e.box;
+    }
+    void run(size_t d, cudaStream_t s, const Box& g) {
+        size_t lo, hi;
+        shard_bounds(n, D, d, lo, hi);
+        aidw_run_config c = cfg;
+        if (!c.use_bbox) {
+            c.use_bbox = 1;
+            c.bbox[0] = g.min_x;
+            c.bbox[1] = g.min_y;
+            c.bbox[2] = g.max_x;
+            c.bbox[3] = g.max_y;
+        }
+        PipelineIO io{b[d].dx.get(), b[d].dy.get(), b[d].dz.get(), b[d].qx.get(), b[d].qy.get(),
+                      m, hi - lo, b[d].pred.get(), b[d].alpha.get()};
+        pipeline_entry(io, c, &st[d], s, b[d].h2d_ms, t0, pred_out + lo,
+                       alpha_out ? alpha_out + lo : nullptr);
+    }
+};
+
+bool pipeline_multi(const std::vector<int>& devs, const double* dx, const double* dy,
+                    const double* dz, size_t m, const double* qx, const double* qy, size_t n,
+                    const aidw_run_config& cfg, double* pred_out, double* alpha_out,
+                    aidw_run_stats* stats, std::chrono::steady_clock::time_point t0) {
+    const size_t D = devs.size();
+    std::unique_ptr<ShardBufs[]> bufs(new ShardBufs[D]);
+    std::unique_ptr<aidw_run_stats[]> st(new aidw_run_stats[D]());
+    PipelineShards job{dx, dy, dz, qx, qy, m, n, D, cfg, pred_out, alpha_out, t0, bufs.get(), st.get()};
+    PipelineShards* j = &job;
+    ShardBufs* b = bufs.get();
+    const bool ok = run_sharded(
+        devs, [j](size_t d, cudaStream_t s) { return j->prep(d, s); },
+        [j](size_t d, cudaStream_t s, const Box& g) { j->run(d, s, g); },
+        [b](size_t d) { b[d].release(); });
+    if (ok && stats) merge_stats(*stats, st.get(), D);
+    return ok;
+}
+
+// run_raster over lattice-row shards, one per listed device.
+struct RasterShards {
+    const double *dx, *dy, *dz;
+    size_t m, nx, ny, D;
+    aidw_run_config cfg;
+    double *raster_out, *alpha_out;
+    std::chrono::steady_clock::time_point t0;
+    ShardBufs* b;
+    aidw_run_stats* st;
+
+    Box prep(size_t d, cudaStream_t s) {
+        const auto c0 = std::chrono::steady_clock::now();
+        h2d(b[d].dx, dx, m, s);
+        h2d(b[d].dy, dy, m, s);
+        h2d(b[d].dz, dz, m, s);
+        const Extents e = extents(b[d].dx.get(), b[d].dy.get(), m, nullptr, nullptr, 0, nullptr, 0, s);
+        b[d].h2d_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+        return e.box;
+    }
+    void run(size_t d, cudaStream_t s, const Box& g) {
+        size_t r0, r1;
+        shard_bounds(ny, D, d, r0, r1);
+        const size_t n = nx * (r1 - r0);
+        const double bb[4] = {g.min_x, g.min_y, g.max_x, g.max_y};
+        b[d].qx.alloc(n, s);
+        b[d].qy.alloc(n, s);
+        b[d].pred.alloc(n, s);
+        b[d].alpha.alloc(n, s);
+        lattice_device(nx, ny, bb, r0, r1 - r0, b[d].qx.get(), b[d].qy.get(), s);
+        aidw_run_config c = cfg;
+        c.use_bbox = 1;
+        std::memcpy(c.bbox, bb, sizeof bb);
+        PipelineIO io{b[d].dx.get(), b[d].dy.get(), b[d].dz.get(), b[d].qx.get(), b[d].qy.get(),
+                      m, n, b[d].pred.get(), b[d].alpha.get()};
+        pipeline_entry(io, c, &st[d], s, b[d].h2d_ms, t0, raster_out + nx * r0,
+                       alpha_out ? alpha_out + nx * r0 : nullptr);
+    }
+};
+
+bool raster_multi(const std::vector<int>& devs, const double* dx, const double* dy,
+                  const double* dz, size_t m, size_t nx, size_t ny, const aidw_run_config& cfg,
+                  double* raster_out, double* alpha_out, double* bbox_out, aidw_run_stats* stats,
+                  std::chrono::steady_clock::time_point t0) {
+    const size_t D = devs.size();
+    std::unique_ptr<ShardBufs[]> bufs(new ShardBufs[D]);
+    std::unique_ptr<aidw_run_stats[]> st(new aidw_run_stats[D]());
+    std::unique_ptr<Box[]> box(new Box[1]);
+    RasterShards job{dx, dy, dz, m, nx, ny, D, cfg, raster_out, alpha_out, t0, bufs.get(), st.get()};
+    RasterShards* j = &job;
+    ShardBufs* b = bufs.get();
+    Box* kept = box.get();
+    const bool ok = run_sharded(
+        devs, [j](size_t d, cudaStream_t s) { return j->prep(d, s); },
+        [j, kept](size_t d, cudaStream_t s, const Box& g) {
+            if (d == 0) *kept = g;
+            j->run(d, s, g);
+        },
+        [b](size_t d) { b[d].release(); });
+    if (ok) {
+        if (stats) merge_stats(*stats, st.get(), D);
+        if (bbox_out) {
+            bbox_out[0] = kept->min_x;
+            bbox_out[1] = kept->min_y;
+            bbox_out[2] = kept->max_x;
+            bbox_out[3] = kept->max_y;
+        }
+    }
+    return ok;
+}
+
 }  // namespace
 }  // namespace aidwb
 
@@ -885,6 +1176,27 @@ int aidw_idw_predict_all(const double* qx, const double* qy, size_t n, const dou
     });
 }
 
+int aidw_set_devices(const int32_t* ids, int32_t count, aidw_error* err) {
+    return guarded(err, [&] {
+        int have = 0;
+        CK(cudaGetDeviceCount(&have));
+        std::vector<int> v;
+        for (int32_t i = 0; i < count; ++i) {
+            if (!ids || ids[i] < 0 || ids[i] >= have)
+                throw Failure(AIDW_ERR_INVALID_ARGUMENT, "set_devices: no such device");
+            v.push_back(ids[i]);
+        }
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        g_dev_env_read = true;
+        g_devices = v;
+    });
+}
+
+int32_t aidw_device_count(void) {
+    const auto d = device_list();
+    return static_cast<int32_t>(d.size() > 1 ? d.size() : 1);
+}
+
 int aidw_run_pipeline(const double* dx, const double* dy, const double* dz, size_t m,
                       const double* qx, const double* qy, size_t n, const aidw_run_config* cfg,
                       double* pred_out, double* alpha_out, aidw_run_stats* stats,
@@ -892,6 +1204,12 @@ int aidw_run_pipeline(const double* dx, const double* dy, const double* dz, size
     return guarded(err, [&] {
         if (!cfg) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "run_pipeline: config missing");
         const auto t0 = std::chrono::steady_clock::now();
+        const std::vector<int> devs = device_list();
+        if (devs.size() > 1 && n >= devs.size() && m > 0 && dz) {
+            if (pipeline_multi(devs, dx, dy, dz, m, qx, qy, n, *cfg, pred_out, alpha_out, stats, t0))
+                return;
+            CK(cudaSetDevice(devs[0]));  // a shard failed: one-device run raises the exact error
+        }
         StreamScope ss;
         cudaStream_t s = ss.s;
         DBuf<double> ddx, ddy, ddz, dqx, dqy, pred(n, s), alpha(n, s);
@@ -941,6 +1259,13 @@ int aidw_run_raster(const double* dx, const double* dy, const double* dz, size_t
             throw Failure(AIDW_ERR_INVALID_ARGUMENT, "cmd_raster: nx and ny must be >= 1");
         if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "cmd_raster: data set is empty");
         const auto t0 = std::chrono::steady_clock::now();
+        const std::vector<int> devs = device_list();
+        if (devs.size() > 1 && ny >= devs.size() && dz) {
+            if (raster_multi(devs, dx, dy, dz, m, nx, ny, *cfg, raster_out, alpha_out, bbox_out,
+                             stats, t0))
+                return;
+            CK(cudaSetDevice(devs[0]));  // a shard failed: one-device run raises the exact error
+        }
         StreamScope ss;
         cudaStream_t s = ss.s;
         const size_t n = nx * ny;
