@@ -363,8 +363,12 @@ def main():
         def e2e_call():
             return A.run_raster(hd, 4096, 4096, rcfg, with_alpha=False)
     else:
+        # results land in pinned host buffers (the C-ABI writes caller memory)
+        pout = (torch.empty(n, dtype=torch.float64).pin_memory().numpy(),
+                torch.empty(n, dtype=torch.float64).pin_memory().numpy())
+
         def e2e_call():
-            return A.run_pipeline(hd, hq, hcfg)
+            return A.run_pipeline(hd, hq, hcfg, out=pout)
     e2e_call()
     barrier()
     t0 = time.perf_counter()

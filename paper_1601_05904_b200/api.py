@@ -388,10 +388,18 @@ def idw_predict_all(queries: PointSet, data: PointSet, alpha: float, variant: st
     return InterpolationResult(pred, alph)
 
 
-def run_pipeline(data: PointSet, queries: PointSet, cfg: RunConfig) -> PipelineOutcome:
-    """cli::run_pipeline (cli.hpp:217-268), fused on the GPU; host buffers."""
+def run_pipeline(data: PointSet, queries: PointSet, cfg: RunConfig, out=None) -> PipelineOutcome:
+    """cli::run_pipeline (cli.hpp:217-268), fused on the GPU; host buffers.
+    `out` = optional (pred, alpha) float64 arrays of length n to write into
+    (e.g. pinned host memory, as the C-ABI allows)."""
     n = queries.count()
-    pred, alph = np.empty(n), np.empty(n)
+    if out is not None:
+        pred, alph = out
+        if pred.dtype != np.float64 or alph.dtype != np.float64 or len(pred) != n or \
+                len(alph) != n or not pred.flags.c_contiguous or not alph.flags.c_contiguous:
+            raise InvalidArgument("run_pipeline: out arrays must be contiguous float64 of length n")
+    else:
+        pred, alph = np.empty(n), np.empty(n)
     st = L.RunStats()
     c = cfg.c()
     err = L.Error()
