@@ -20,6 +20,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "weight.cuh"
@@ -43,8 +44,8 @@ __device__ __forceinline__ double recipe_denominator(double d2, int n4) {
     return den;
 }
 
-// One thread carries QT queries (visiting positions p, p + 128, ...), so a
-// broadcast shared-memory read of one data point feeds QT pairs; the data
+// One thread carries QT queries (visiting positions p, p + 128, ...; QT = 1
+// by default, more warps beat per-thread ILP for the FP64 chains); the data
 // stream through shared memory in index order, 256-point tiles.  The snap
 // index and the nearest index come from the k = 1 grid search (FP64, the
 // same d2 as here: identical first-index / lowest-index semantics), so the
@@ -84,8 +85,13 @@ __global__ void fp64_order_kernel(const uint32_t* __restrict__ flag,
     order[slot] = static_cast<uint32_t>(p);
 }
 
+#ifndef AIDW_FP64_THREADS
+#define AIDW_FP64_THREADS 256
+#endif
+constexpr int kFp64Threads = AIDW_FP64_THREADS;
+
 template <bool BLOCKED, int QT>
-__global__ void __launch_bounds__(128) weight_fp64_kernel(const WeightQueries q,
+__global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQueries q,
                                                           const WeightFrame f,
                                                           const WeightData d,
                                                           const uint32_t* __restrict__ order,
@@ -204,10 +210,15 @@ void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFra
     if (q.n == 0) return;
     if (!q.snap_s || !q.nn_s)
         throw Failure(AIDW_ERR_RUNTIME, "weighting_fp64: nearest / snap indices missing");
-    // queries per thread: 4 once that still leaves ~8 CTAs per SM, else
-    // fewer (the per-query arithmetic and order are the same for any QT)
-    const size_t per_sm = 8 * 148 * 128;
-    const int qt = q.n >= 4 * per_sm ? 4 : (q.n >= 2 * per_sm ? 2 : 1);
+    // queries per thread: 1 (measured at 1M x 1M: 1.18 s vs 1.32 s at 2 and
+    // 1.79 s at 4 — the FP64 chains need warps more than per-thread ILP);
+    // the per-query arithmetic and order are the same for any QT
+    int qt = 1;
+    static const int force_qt = [] {  // AIDW_FP64_QT: tuning experiments
+        const char* v = std::getenv("AIDW_FP64_QT");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (force_qt == 1 || force_qt == 2 || force_qt == 4) qt = force_qt;
     DBuf<uint32_t> flag(q.n, s), scan(q.n, s), order(q.n, s);
     LAUNCH(fp64_class_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, blocked ? 1 : 0,
            flag.get());
@@ -216,7 +227,8 @@ void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFra
            order.get());
     auto go = [&](auto kernel, int k) {
         if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
-        LAUNCH(kernel, ceil_div(q.n, static_cast<size_t>(128 * k)), 128, 0, s, q, f, d,
+        LAUNCH(kernel, ceil_div(q.n, static_cast<size_t>(kFp64Threads * k)), kFp64Threads, 0, s,
+               q, f, d,
                order.get(), d_pred, d_alpha);
     };
     if (blocked) {
