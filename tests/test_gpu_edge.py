@@ -172,3 +172,18 @@ def test_deterministic_and_shard_invariant():
         assert np.array_equal(part.alphas, full.alphas[lo:hi])
     again = A.run_pipeline(data, q, cfg).result
     assert np.array_equal(again.predicted, full.predicted)
+
+
+@pytest.mark.parametrize("m", [2, 255, 256, 257, 2047, 2048, 2049, 4097, 262_144, 262_145])
+def test_tile_and_chunk_boundaries(m):
+    """Data sizes at the K4 tile (256), chunk-split (8 tiles per chunk, 64
+    chunks up to 1024 tiles, 16 beyond) and nearest-search grid (4096)
+    boundaries: partial last tiles are NEAR with exact-zero pads, every
+    chunk is folded once — predictions within the contract, alpha exact."""
+    data = A.generate_random_points(m, UNIT, 31)
+    q = A.generate_random_queries(257, UNIT, 32)
+    k = min(10, m)
+    out = A.run_pipeline(data, q, A.RunConfig(params=A.AidwParams(k=10)))
+    ref = O.pipeline(data.xs, data.ys, data.zs, q.xs, q.ys, k=k, variant=1)
+    assert np.max(np.abs(out.result.alphas - ref["alpha"]) / ref["alpha"]) <= 1e-12
+    assert pred_err(out.result.predicted, ref["pred"], data.zs) <= 1e-5
