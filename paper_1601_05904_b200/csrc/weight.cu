@@ -3,24 +3,28 @@
 // Replaces the weighting loops of aidw_predict_all / idw_predict_all
 // (proj/include/aidw/interpolate.hpp:252-381, :426-489).  Design:
 //
-//  * Data records live in HBM as {x_hi, y_hi, x_lo, y_lo} float4 + z float,
-//    coordinates normalised to the unit box in FP64 first and split into an
-//    FP32 hi/lo pair, so dx = (x_hi - q_hi) + (x_lo - q_lo) keeps ~48 bits
-//    without any FP64 op or F2F conversion per pair.  Padded to 256-point
-//    tiles with records at 1e30 (weight exactly 0).
-//  * Each CTA (256 threads, QT queries per thread in registers) streams the
-//    tiles of one data chunk through a NSTAGE-deep shared-memory ring filled
+//  * Data records: 256-point tiles of 9 SoA float components in 8 x 8-cell
+//    block order of the factor-4 grid (compact squares): x / y / z as FP32
+//    hi/lo pairs of the unit-box-normalised FP64 values (the NEAR form,
+//    dx = (x_hi - q_hi) + (x_lo - q_lo), ~48 bits, no FP64 op or F2F per
+//    pair) and the tile-centred FAR form -2 p'x, -2 p'y, |p'|^2 (d2 in three
+//    FP32 ops).  Padded records weigh exactly 0 in the near form, the only
+//    one a partial tile uses.
+//  * Each CTA (256 threads, 4 queries per thread as two f32x2 pairs) streams
+//    the tiles of one data chunk through a 4-stage shared-memory ring filled
 //    by the bulk-copy engine (cp.async.bulk + mbarrier complete_tx; SASS
-//    UBLKCP), one elected thread producing, all warps consuming broadcast
-//    LDS.128 reads.
-//  * Ratio scaling: w' = (d2 / d2_min)^(-alpha/2) <= 1, evaluated as
-//    ex2(c * lg2(d2) + b) with c = -alpha/2, b = -c * lg2(d2_min) — two MUFU
-//    ops (MUFU.LG2, MUFU.EX2) + 9 FP32 ops per pair.  Queries with
-//    alpha == 4 exactly (98 % of uniform-data queries, the reference's
-//    half-integer recipe, interpolate.hpp:174-209) use w' = rcp((d2*s)^2),
-//    one MUFU.  Queries are partitioned so warps are class-uniform; the
-//    formula is chosen per query, never per warp, so results do not depend
-//    on the partition (or on the GPU count).
+//    UBLKCP); the last warp done with a stage refills it, so warps drift
+//    instead of meeting at a barrier.  Queries are visited in Morton order.
+//  * Per (query, tile): FAR when the query's distance to the tile's box
+//    exceeds max(R_far, half the tile diagonal), else NEAR (Kahan-compensated
+//    sums with hi/lo z).  A function of the (query, tile) pair only.
+//  * Weights: general alpha, ratio-scaled w' = (d2 / d2_min)^(-alpha/2) =
+//    ex2(c lg2(d2) + b) (G1: MUFU ex2; G2: ex2 as a degree-6 polynomial on
+//    the FMA pipe, interleaved 1:1 per warp); alpha == 4 exactly (98 % of
+//    uniform-data queries, the reference's half-integer recipe,
+//    interpolate.hpp:174-209): w' = 1 / (d2 s)^2, and in far tiles two of
+//    every four points share one reciprocal.  One launch serves both classes
+//    (general CTAs first); the formula is chosen per query, never per warp.
 //  * Per-tile FP32 sums are folded into FP64 accumulators; data chunks
 //    (S = f(m) only) give enough CTAs at small n and are summed in chunk
 //    order by the settle kernel, deterministically (no atomics).
