@@ -238,10 +238,17 @@ def main():
     import paper_1601_05904_b200 as A
 
     world, rank, local = dist_env()
+    # AIDW_BENCH_SHARED_DEVICE=1 (test hook): every rank on device 0 with the
+    # gloo backend, so the multi-rank path runs end to end on a one-GPU box
+    shared = os.environ.get("AIDW_BENCH_SHARED_DEVICE") == "1"
+    local = 0 if shared else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
