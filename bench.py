@@ -1,7 +1,7 @@
 """bench.py — interpolated points/s of the fused AIDW pipeline on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 1m|clustered|100k|dem] [--no-cpu-baseline]
+                    [--config 1m|clustered|100k|paper|dem] [--no-cpu-baseline]
 
 A step = one full pass of the hot path (bbox -> grid build K1 -> query sort
 -> kNN + alpha K2/K3 -> weighting K4 -> settle) over one batch: m = 1M data
@@ -39,6 +39,8 @@ CONFIGS = {
                       workload="1M x 1M per rank, 20 Gaussian blobs sigma=0.03, k=10 (BASELINE configs[3])"),
     "100k": dict(m=100_000, n=100_000, k=10, dist="uniform",
                  workload="100K x 100K uniform, k=10 (BASELINE configs[1])"),
+    "paper": dict(m=1_024_000, n=1_024_000, k=10, dist="uniform",
+                  workload="1000K x 1000K uniform (the paper's rung, 1K = 1024; SURVEY §8d), k=10"),
     "dem": dict(m=4_000_000, n=4096 * 4096, k=15, dist="lattice",
                 workload="4M planar data x 4096^2 raster lattice, k=15 (BASELINE configs[4])"),
 }
