@@ -250,8 +250,8 @@ __device__ __forceinline__ void finish_query(const KnnArgs& a, TopK& t, size_t p
 // The next candidate's coordinates and id are loaded one iteration ahead.
 template <class TopK>
 __device__ __forceinline__ void scan_row(const KnnArgs& a, TopK& t, double qx, double qy,
-                                         double fx, double fy, double w2, int rr, int c0, int c1,
-                                         uint32_t& snap, unsigned long long& scanned) {
+                                         double fx, double fy, double inv_w2, int rr, int c0,
+                                         int c1, uint32_t& snap, unsigned long long& scanned) {
     const int n_col = a.g.n_col, n_row = a.g.n_row;
     if (t.full()) {
         const double inf = __longlong_as_double(0x7FF0000000000000ll);
@@ -259,9 +259,13 @@ __device__ __forceinline__ void scan_row(const KnnArgs& a, TopK& t, double qx, d
         const double thr = fmax(t.kth(), a.snap_sq);
         const double y0 = rr == 0 ? -inf : rr - pad, y1 = rr == n_row - 1 ? inf : rr + 1 + pad;
         const double dy = fmax(0.0, fmax(y0 - fy, fy - y1));
-        const double room = thr / (w2 * (1.0 - 1.0e-9)) - dy * dy;  // dx^2 budget, cell units
+        // dx^2 budget in cell units; inv_w2 = 1 / (w2 (1 - 1e-9)) rounded up
+        // by a further 1e-12, so room only ever errs high
+        const double room = thr * inv_w2 - dy * dy;
         if (room < 0.0) return;  // the whole row is strictly worse
-        const double h = sqrt(room) * (1.0 + 1.0e-9) + 1.0e-9;
+        // the reach in FP32 (MUFU sqrt), overestimated by 1e-5 relative +
+        // 1e-4 cells: trimming keeps a superset of the exact test's cells
+        const double h = static_cast<double>(sqrtf(__double2float_ru(room)) * 1.00001f + 1.0e-4f);
         // cell c is kept iff c - pad - fx <= h and fx - (c + 1 + pad) <= h;
         // the edge cells are unbounded outward (keep them on their open side)
         const double lo = floor(fx - h - pad - 1.0), hi = floor(fx + h + pad);
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
         const double fx = __ddiv_rn(__dsub_rn(qx, a.g.min_x), a.g.cell_width);
         const double fy = __ddiv_rn(__dsub_rn(qy, a.g.min_y), a.g.cell_width);
         const double w2 = __dmul_rn(a.g.cell_width, a.g.cell_width);
+        const double inv_w2 = (1.0 / (w2 * (1.0 - 1.0e-9))) * (1.0 + 1.0e-12);
         // The reference scans the whole level block at once; scanning it row
         // by row outward from the query's row and trimming each row to the
         // cells that can still hold a point below the current k-th yields the
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
             for (int d = 0; d <= 2 * level; ++d) {
                 const int rr = row + ((d & 1) ? -((d + 1) >> 1) : (d >> 1));
                 if (rr < 0 || rr >= n_row) continue;
-                scan_row(a, t, qx, qy, fx, fy, w2, rr, c0, c1, snap, scanned);
+                scan_row(a, t, qx, qy, fx, fy, inv_w2, rr, c0, c1, snap, scanned);
             }
         }
         // ring widening (knn.hpp:234-247, scan_ring :175-194)
@@ -353,16 +358,16 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
             ++level;
             const int r = level;
             const int c0 = imax(0, col - r), c1 = imin(n_col - 1, col + r);
-            if (row - r >= 0) scan_row(a, t, qx, qy, fx, fy, w2, row - r, c0, c1, snap, scanned);
+            if (row - r >= 0) scan_row(a, t, qx, qy, fx, fy, inv_w2, row - r, c0, c1, snap, scanned);
             if (row + r <= n_row - 1)
-                scan_row(a, t, qx, qy, fx, fy, w2, row + r, c0, c1, snap, scanned);
+                scan_row(a, t, qx, qy, fx, fy, inv_w2, row + r, c0, c1, snap, scanned);
             const int r0 = imax(0, row - r + 1), r1 = imin(n_row - 1, row + r - 1);
             if (col - r >= 0)
                 for (int rr = r0; rr <= r1; ++rr)
-                    scan_row(a, t, qx, qy, fx, fy, w2, rr, col - r, col - r, snap, scanned);
+                    scan_row(a, t, qx, qy, fx, fy, inv_w2, rr, col - r, col - r, snap, scanned);
             if (col + r <= n_col - 1)
                 for (int rr = r0; rr <= r1; ++rr)
-                    scan_row(a, t, qx, qy, fx, fy, w2, rr, col + r, col + r, snap, scanned);
+                    scan_row(a, t, qx, qy, fx, fy, inv_w2, rr, col + r, col + r, snap, scanned);
         }
         if (a.ref_candidates) {  // what the reference scanned: the final-level block
             ref_scanned = rect_count(a, imax(0, col - level), imin(n_col - 1, col + level),
