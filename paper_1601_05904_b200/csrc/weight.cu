@@ -47,7 +47,13 @@ namespace aidwb {
 
 namespace {
 
-constexpr int kK4Threads = 256;
+#ifndef AIDW_K4_THREADS
+#define AIDW_K4_THREADS 256
+#endif
+#ifndef AIDW_K4_MINB
+#define AIDW_K4_MINB 2
+#endif
+constexpr int kK4Threads = AIDW_K4_THREADS;
 #ifndef AIDW_K4_STAGES
 #define AIDW_K4_STAGES 4
 #endif
@@ -964,7 +970,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     switch (variant) {
         case 1: launch(weight_fp32_kernel<4, 3>, 4); break;
         case 2: launch(weight_fp32_kernel<2, 4>, 2); break;
-        default: launch(weight_fp32_kernel<4, 2>, 4); break;
+        default: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;
     }
     if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
     LAUNCH(settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order_q.get(),
