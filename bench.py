@@ -415,6 +415,13 @@ def main():
                                      f"0.75 MUFU) and general alpha (MUFU-bound 10.5 FP32 + "
                                      f"1.5 MUFU) far-tile forms; 128 FP32 + 16 MUFU per SM-clk",
                          "frac_vs_2mufu_roofline": achieved / peak_gpairs,
+                         "fp32_view": {  # the same bound as FP32 op throughput
+                             "unit": "TFLOP/s (FP32 ops, FFMA = 1)",
+                             "ops_per_pair": (a4 * 6.5 + (n - a4) * 10.5) / n,
+                             "achieved": achieved * 1e9 * (a4 * 6.5 + (n - a4) * 10.5) / n / 1e12,
+                             "peak": sms * 128 * f_mhz * 1e6 / 1e12,
+                             "frac": achieved * 1e9 * (a4 * 6.5 + (n - a4) * 10.5) / n /
+                                     (sms * 128 * f_mhz * 1e6)},
                          "alpha4_recipe_queries": a4, "pairs_per_launch": pairs,
                          "k4_ms": k4_ms},
             "roofline_general_alpha": {"bound": "fp32+mufu pipes (MUFU-bound)",
