@@ -54,6 +54,10 @@ namespace {
 #define AIDW_K4_MINB 2
 #endif
 constexpr int kK4Threads = AIDW_K4_THREADS;
+#ifndef AIDW_K4_FAR_UNROLL
+#define AIDW_K4_FAR_UNROLL 2
+#endif
+constexpr int kFarUnroll = AIDW_K4_FAR_UNROLL;  // 4-point groups per far-loop trip
 #ifndef AIDW_K4_STAGES
 #define AIDW_K4_STAGES 4
 #endif
@@ -515,7 +519,7 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
                                        const f2 (&fq)[QT / 2], f2 (&sw)[QT / 2],
                                        f2 (&swz)[QT / 2]) {
     constexpr int kPairs = QT / 2;
-#pragma unroll 2
+#pragma unroll kFarUnroll
     for (int j = 0; j < kWeightTile; j += 4) {
         const float4 X = *reinterpret_cast<const float4*>(t + kPX * kWeightTile + j);
         const float4 Y = *reinterpret_cast<const float4*>(t + kPY * kWeightTile + j);
