@@ -882,14 +882,18 @@ void set_alpha4_recipe(bool enabled) { g_alpha4_recipe.store(enabled); }
 WeightSplit weight_split(size_t m) {
     // Data chunks per query (the grid's y dimension): enough CTAs to fill
     // 148 SMs at small n without a partial last wave dominating — up to 64
-    // chunks of >= 8 tiles while m <= 256K, 16 chunks beyond (partials stay
+    // chunks of >= 4 tiles while m <= 256K, 16 chunks beyond (partials stay
     // 256 B per query).  A function of m only, so a query's summation order
     // never depends on n, the shard or the GPU count.
     WeightSplit w;
     w.tiles = (m + kWeightTile - 1) / kWeightTile;
     if (w.tiles == 0) w.tiles = 1;
     const size_t cap = w.tiles <= 1024 ? 64 : static_cast<size_t>(kMaxChunks);
-    size_t chunks = std::min(cap, std::max<size_t>(1, w.tiles / 8));
+    static const size_t min_tiles = [] {  // AIDW_K4_CHUNK_TILES: tuning only
+        const char* v = std::getenv("AIDW_K4_CHUNK_TILES");
+        return static_cast<size_t>(v ? std::max(1, std::atoi(v)) : 4);
+    }();
+    size_t chunks = std::min(cap, std::max<size_t>(1, w.tiles / min_tiles));
     if (w.tiles > 1024) chunks = std::min(w.tiles, static_cast<size_t>(kMaxChunks));
     w.tiles_per_chunk = (w.tiles + chunks - 1) / chunks;
     w.chunks = static_cast<unsigned>((w.tiles + w.tiles_per_chunk - 1) / w.tiles_per_chunk);
