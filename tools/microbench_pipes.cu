@@ -3,6 +3,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb microbench_pipes.cu
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #define N_ITER 4096
 typedef unsigned long long u64;
 __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) { u64 r; asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r; }
@@ -15,6 +16,8 @@ __device__ __forceinline__ double rcp64(double x) { double r; asm volatile("rcp.
 
 template <int MODE> __global__ void k(float* out, float s) {
   float a[8]; u64 p[8]; double dd[8]; const double ds = s;
+  __half2 hh[8]; const __half2 hs = __float2half2_rn(s);
+  for (int i = 0; i < 8; ++i) hh[i] = __float2half2_rn(threadIdx.x * 1e-3f + i);
   for (int i = 0; i < 8; ++i) dd[i] = threadIdx.x * 1e-3 + i;
   for (int i = 0; i < 8; ++i) { a[i] = threadIdx.x * 1e-3f + i; p[i] = __float_as_uint(a[i]) | ((u64)__float_as_uint(a[i] + 1.f) << 32); }
   u64 ps = __float_as_uint(s) | ((u64)__float_as_uint(s) << 32);
@@ -33,9 +36,11 @@ template <int MODE> __global__ void k(float* out, float s) {
       if (MODE == 9) dd[i] = dd[i] + ds;                             // DADD
       if (MODE == 10) dd[i] = rcp64(dd[i]);                          // MUFU.RCP64H (+ fixup)
       if (MODE == 11) { dd[i] = fma(dd[i], ds, 0.5); p[i] = ffma2(p[i], ps, ps); }  // DFMA + FFMA2
+      if (MODE == 12) hh[i] = __hfma2(hh[i], hs, hs);                // HFMA2
+      if (MODE == 13) { hh[i] = __hfma2(hh[i], hs, hs); p[i] = ffma2(p[i], ps, ps); }  // HFMA2 + FFMA2
     }
   }
-  float r = 0; for (int i = 0; i < 8; ++i) r += a[i] + __uint_as_float((unsigned)p[i]) + (float)dd[i];
+  float r = 0; for (int i = 0; i < 8; ++i) r += a[i] + __uint_as_float((unsigned)p[i]) + (float)dd[i] + __low2float(hh[i]);
   if (r == 12345.f) out[0] = r;
 }
 int main() {
@@ -43,16 +48,16 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const char* names[] = {"FFMA", "FFMA2", "FADD2", "MUFU.EX2", "MUFU.RCP", "MUFU.LG2", "FFMA2+EX2", "FFMA+FADD",
-                         "DFMA", "DADD", "RCP.F64", "DFMA+FFMA2"};
-  const int ops[] = {1, 1, 1, 1, 1, 1, 2, 2, 1, 1, 1, 2};
+                         "DFMA", "DADD", "RCP.F64", "DFMA+FFMA2", "HFMA2", "HFMA2+FFMA2"};
+  const int ops[] = {1, 1, 1, 1, 1, 1, 2, 2, 1, 1, 1, 2, 1, 2};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int mode = 0; mode < 12; ++mode) {
+  for (int mode = 0; mode < 14; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       dim3 g(sms * 8), b(256);
       cudaEventRecord(e0);
       switch (mode) { case 0: k<0><<<g,b>>>(o,1.0001f); break; case 1: k<1><<<g,b>>>(o,1.0001f); break; case 2: k<2><<<g,b>>>(o,1.0001f); break; case 3: k<3><<<g,b>>>(o,0.5f); break;
         case 4: k<4><<<g,b>>>(o,1.f); break; case 5: k<5><<<g,b>>>(o,1.f); break; case 6: k<6><<<g,b>>>(o,1.0001f); break; case 7: k<7><<<g,b>>>(o,1.0001f); break;
-        case 8: k<8><<<g,b>>>(o,1.0001f); break; case 9: k<9><<<g,b>>>(o,1.0001f); break; case 10: k<10><<<g,b>>>(o,1.f); break; case 11: k<11><<<g,b>>>(o,1.0001f); break; }
+        case 8: k<8><<<g,b>>>(o,1.0001f); break; case 9: k<9><<<g,b>>>(o,1.0001f); break; case 10: k<10><<<g,b>>>(o,1.f); break; case 11: k<11><<<g,b>>>(o,1.0001f); break; case 12: k<12><<<g,b>>>(o,1.0001f); break; case 13: k<13><<<g,b>>>(o,1.0001f); break; }
       cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       double warp_instr = (double)sms * 8 * 8 * N_ITER * 8 * ops[mode];  // warps * iters * unroll * ops
