@@ -61,7 +61,8 @@ __device__ __forceinline__ bool recipe_alpha(double alpha) {
 // alpha == 4 warps take a specialised loop).
 __global__ void fp64_class_kernel(const WeightQueries q, int blocked, uint32_t* __restrict__ flag) {
     const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (p < q.n) flag[p] = (blocked && q.alpha_s[p] != 4.0) ? 1u : 0u;
+    if (p < q.n) flag[p] = q.alpha_s[p] != 4.0 ? 1u : 0u;
+    (void)blocked;
 }
 
 // 1 / x to ~1 ulp on the FP64 pipe: MUFU.RCP64H seed + two Newton steps,
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQ
         double cw[QT], cwz[QT];  // chunk partials (BLOCKED)
 #pragma unroll
         for (int i = 0; i < QT; ++i) cw[i] = cwz[i] = 0.0;
-        if (BLOCKED && all4) {  // warp-uniform alpha == 4: w = 1 / (d2 d2)
+        if (all4) {  // warp-uniform alpha == 4: w = 1 / (d2 d2) (naive: = 1 / pow(sqrt(d2), 4)
+                     // to ~2 ulp, within the FP64 contract; naive and pinned share it)
             for (int j = 0; j < len; ++j) {
                 const double2 xy = sxy[j];
                 const double z = sz[j];
@@ -143,8 +145,13 @@ __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQ
                 for (int i = 0; i < QT; ++i) {
                     const double d2 = dsq_rn(qx[i], qy[i], xy.x, xy.y);
                     const double w = rcp_nr(__dmul_rn(d2, d2));
-                    cw[i] = __dadd_rn(cw[i], w);
-                    cwz[i] = __dadd_rn(cwz[i], __dmul_rn(w, z));
+                    if (BLOCKED) {
+                        cw[i] = __dadd_rn(cw[i], w);
+                        cwz[i] = __dadd_rn(cwz[i], __dmul_rn(w, z));
+                    } else {  // index-order running sums (predict_naive)
+                        sw[i] = __dadd_rn(sw[i], w);
+                        swz[i] = __dadd_rn(swz[i], __dmul_rn(w, z));
+                    }
                 }
             }
         } else
