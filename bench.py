@@ -1,7 +1,7 @@
 """bench.py — interpolated points/s of the fused AIDW pipeline on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 1m|clustered|100k|paper|dem] [--no-cpu-baseline]
+                    [--config 1m|clustered|10k|100k|paper|dem] [--no-cpu-baseline]
 
 A step = one full pass of the hot path (bbox -> grid build K1 -> query sort
 -> kNN + alpha K2/K3 -> weighting K4 -> settle) over one batch: m = 1M data
@@ -37,6 +37,8 @@ CONFIGS = {
                workload="1M data x 1M queries per rank, uniform unit square, k=10 (BASELINE configs[2])"),
     "clustered": dict(m=1_000_000, n=1_000_000, k=10, dist="clustered",
                       workload="1M x 1M per rank, 20 Gaussian blobs sigma=0.03, k=10 (BASELINE configs[3])"),
+    "10k": dict(m=10_000, n=10_000, k=10, dist="uniform",
+                workload="10K x 10K uniform, k=10 (BASELINE configs[0], the reference's serial CPU case)"),
     "100k": dict(m=100_000, n=100_000, k=10, dist="uniform",
                  workload="100K x 100K uniform, k=10 (BASELINE configs[1])"),
     "paper": dict(m=1_024_000, n=1_024_000, k=10, dist="uniform",
