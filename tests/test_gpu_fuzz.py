@@ -40,7 +40,7 @@ def case(seed):
     if rng.random() < 0.3:  # some queries exactly on data sites (snap)
         j = rng.integers(0, m, min(n, 5))
         qx[:j.size], qy[:j.size] = xs[j], ys[j]
-    k = int(rng.choice([1, 3, 10, 15, 24]))
+    k = int(rng.choice([1, 3, 10, 15, 24, 70]))
     factor = float(rng.choice([1.0, 2.0, 4.0, 8.0]))
     r_max = float(rng.choice([1.5, 2.0, 3.0]))
     engine = str(rng.choice(["grid", "brute"]))
