@@ -91,13 +91,15 @@ __global__ void fp64_order_kernel(const uint32_t* __restrict__ flag,
 #endif
 constexpr int kFp64Threads = AIDW_FP64_THREADS;
 
+// Each CTA covers QT x blockDim queries against ONE data chunk (blockIdx.y:
+// points [chunk * chunk_pts, +chunk_pts), chunking a function of m only) and
+// writes its FP64 partial sums; fp64_settle_kernel adds the chunks in order.
 template <bool BLOCKED, int QT>
 __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQueries q,
-                                                          const WeightFrame f,
                                                           const WeightData d,
                                                           const uint32_t* __restrict__ order,
-                                                          double* __restrict__ pred,
-                                                          double* __restrict__ alpha_out) {
+                                                          size_t chunk_pts,
+                                                          double2* __restrict__ part) {
     __shared__ double2 sxy[kTile64];
     __shared__ double sz[kTile64];
     const size_t p0 = static_cast<size_t>(blockIdx.x) * blockDim.x * QT + threadIdx.x;
@@ -125,8 +127,10 @@ __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQ
 #pragma unroll
     for (int i = 0; i < QT; ++i) four &= alpha[i] == 4.0;
     const bool all4 = __all_sync(0xFFFFFFFFu, four);
-    for (size_t base = 0; base < d.m; base += kTile64) {
-        const int len = static_cast<int>(d.m - base < kTile64 ? d.m - base : kTile64);
+    const size_t c0 = static_cast<size_t>(blockIdx.y) * chunk_pts;
+    const size_t c1 = c0 + chunk_pts < d.m ? c0 + chunk_pts : d.m;
+    for (size_t base = c0; base < c1; base += kTile64) {
+        const int len = static_cast<int>(c1 - base < kTile64 ? c1 - base : kTile64);
         __syncthreads();
         for (int j = threadIdx.x; j < len; j += blockDim.x) {
             sxy[j] = make_double2(d.x[base + j], d.y[base + j]);
@@ -184,29 +188,46 @@ __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQ
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
         const size_t slot = p0 + static_cast<size_t>(i) * blockDim.x;
-        if (slot >= q.n) continue;
-        const size_t p = order[slot];
-        const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
-        double out;
-        const uint32_t snap = q.snap_s[p];
-        if (snap != kNoId) {
-            out = d.z[snap];  // first index within snap distance
-        } else {
-            // settle (interpolate.hpp:109-118)
-            bool ok = false;
-            out = 0.0;
-            if (sw[i] > 0.0 && isfinite(sw[i]) && isfinite(swz[i])) {
-                const double v = __ddiv_rn(swz[i], sw[i]);
-                if (isfinite(v)) {
-                    out = v < f.zlo ? f.zlo : (v > f.zhi ? f.zhi : v);
-                    ok = true;
-                }
-            }
-            if (!ok) out = d.z[q.nn_s[p]];  // nearest_value: lowest index on ties
-        }
-        pred[qi] = out;
-        if (alpha_out) alpha_out[qi] = alpha[i];
+        if (slot < q.n) part[static_cast<size_t>(blockIdx.y) * q.n + slot] = make_double2(sw[i], swz[i]);
     }
+}
+
+// Chunk partials added in chunk order, then the reference's settle
+// (interpolate.hpp:109-118): snap -> z[first index within snap distance];
+// non-finite or non-positive sums -> nearest value (lowest index on ties);
+// clamp to the value hull.
+__global__ void fp64_settle_kernel(const WeightQueries q, const WeightFrame f, const WeightData d,
+                                   const uint32_t* __restrict__ order,
+                                   const double2* __restrict__ part, unsigned chunks,
+                                   double* __restrict__ pred, double* __restrict__ alpha_out) {
+    const size_t slot = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (slot >= q.n) return;
+    const size_t p = order[slot];
+    const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
+    double out;
+    const uint32_t snap = q.snap_s[p];
+    if (snap != kNoId) {
+        out = d.z[snap];
+    } else {
+        double sw = 0.0, swz = 0.0;
+        for (unsigned c = 0; c < chunks; ++c) {
+            const double2 v = part[static_cast<size_t>(c) * q.n + slot];
+            sw = __dadd_rn(sw, v.x);
+            swz = __dadd_rn(swz, v.y);
+        }
+        bool ok = false;
+        out = 0.0;
+        if (sw > 0.0 && isfinite(sw) && isfinite(swz)) {
+            const double v = __ddiv_rn(swz, sw);
+            if (isfinite(v)) {
+                out = v < f.zlo ? f.zlo : (v > f.zhi ? f.zhi : v);
+                ok = true;
+            }
+        }
+        if (!ok) out = d.z[q.nn_s[p]];
+    }
+    pred[qi] = out;
+    if (alpha_out) alpha_out[qi] = q.alpha_s[p];
 }
 
 }  // namespace
@@ -232,11 +253,16 @@ void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFra
     exclusive_scan_u32(flag.get(), scan.get(), q.n, s);
     LAUNCH(fp64_order_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, flag.get(), scan.get(), q.n,
            order.get());
+    // data chunks: the FP32 path's split (a function of m only) — enough CTAs
+    // at small n (100K x 100K: 391 query blocks x 64 chunks)
+    const WeightSplit sp = weight_split(d.m);
+    const size_t chunk_pts = sp.tiles_per_chunk * static_cast<size_t>(kWeightTile);
+    const unsigned chunks = static_cast<unsigned>((d.m + chunk_pts - 1) / chunk_pts);
+    DBuf<double2> part(static_cast<size_t>(chunks) * q.n, s);
     auto go = [&](auto kernel, int k) {
         if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
-        LAUNCH(kernel, ceil_div(q.n, static_cast<size_t>(kFp64Threads * k)), kFp64Threads, 0, s,
-               q, f, d,
-               order.get(), d_pred, d_alpha);
+        const dim3 grid(ceil_div(q.n, static_cast<size_t>(kFp64Threads * k)), chunks);
+        LAUNCH(kernel, grid, kFp64Threads, 0, s, q, d, order.get(), chunk_pts, part.get());
     };
     if (blocked) {
         if (qt == 4) go(weight_fp64_kernel<true, 4>, 4);
@@ -248,6 +274,8 @@ void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFra
         else go(weight_fp64_kernel<false, 1>, 1);
     }
     if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
+    LAUNCH(fp64_settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order.get(),
+           part.get(), chunks, d_pred, d_alpha);
 }
 
 }  // namespace aidwb
