@@ -9,10 +9,9 @@ FP64 weighting mode (AIDW_WEIGHT_FP64=1) must pass everything the
 reference's suites assert.  In the default FP32 mode the only permitted
 failures are the two tolerances SURVEY §8a shows no FP32 kernel can meet
 (blocked-vs-naive 1e-6 at 1000x1000, translation invariance 1e-9), plus the
-acceptance gate's relative-timing criteria 6/7 (and 8 in FP64 mode), which
-compare host-side KnnResult materialisation and transfers against GPU stages
-that are 100x faster than the CPU stages those ratios were written for
-(SURVEY §7.4).  All correctness criteria (1-5, 9, 10) must pass.
+acceptance gate's relative-timing criteria 6/7, which compare host-side
+KnnResult materialisation and transfers against GPU stages that are 100x
+faster than the CPU stages those ratios were written for.  All correctness criteria (1-5, 9, 10) must pass.
 """
 import os
 import subprocess
@@ -77,7 +76,7 @@ def acceptance_failures(out):
 def test_reference_acceptance_fp64():
     rc, out = run("acceptance", {"AIDW_WEIGHT_FP64": "1"}, timeout=1800)
     print(out)
-    assert acceptance_failures(out) <= {6, 7, 8}, out
+    assert acceptance_failures(out) <= {6, 7}, out
 
 
 @pytest.mark.gpu
