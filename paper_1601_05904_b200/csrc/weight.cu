@@ -985,6 +985,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
         case 1: launch(weight_fp32_kernel<4, 3>, 4); break;
         case 2: launch(weight_fp32_kernel<2, 4>, 2); break;
         case 3: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;
+        case 4: launch(weight_fp32_kernel<2, 3>, 2); break;
         default: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;
     }
     if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
