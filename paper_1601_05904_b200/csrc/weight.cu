@@ -54,6 +54,9 @@ namespace {
 #define AIDW_K4_MINB 2
 #endif
 constexpr int kK4Threads = AIDW_K4_THREADS;
+#ifndef AIDW_K4_NEAR_KAHAN_SW
+#define AIDW_K4_NEAR_KAHAN_SW 1
+#endif
 #ifndef AIDW_K4_FAR_UNROLL
 #define AIDW_K4_FAR_UNROLL 2
 #endif
@@ -271,14 +274,22 @@ __global__ void morton_keys_kernel(const WeightQueries q, WeightFrame f, uint32_
 // Flags by Morton rank j (p = zpos[j]).
 __global__ void class_flags_kernel(const WeightQueries q, WeightFrame f, int recipe,
                                    unsigned g2_threshold, const uint32_t* __restrict__ zpos,
-                                   uint32_t* __restrict__ flag_a, uint32_t* __restrict__ flag_g2) {
+                                   uint32_t* __restrict__ flag_a, uint32_t* __restrict__ flag_a2,
+                                   uint32_t* __restrict__ flag_g2) {
     const size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= q.n) return;
     const size_t p = zpos[j];
     const double d2n = q.d2min_s[p] * f.inv_scale * f.inv_scale;
-    const bool a = (recipe && q.alpha_s[p] == 4.0 && d2n >= kRecipeMinD2) || q.snap_s[p] != kNoId;
+    const bool snapped = q.snap_s[p] != kNoId;
+    const double alpha = q.alpha_s[p];
+    // recipe classes: alpha == 4 (w = 1 / d^4) and alpha == 2 (w = 1 / d^2;
+    // the reference's default IDW exponent), both half-integer recipes
+    // (interpolate.hpp:174-209)
+    const bool a2 = recipe && !snapped && alpha == 2.0 && d2n >= kRecipeMinD2;
+    const bool a = (recipe && alpha == 4.0 && d2n >= kRecipeMinD2) || snapped || a2;
     const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
     flag_a[j] = a ? 1u : 0u;
+    flag_a2[j] = a2 ? 1u : 0u;
     const float xh = __double2float_rn((q.qx[qi] - f.ox) * f.inv_scale);
     const float yh = __double2float_rn((q.qy[qi] - f.oy) * f.inv_scale);
     flag_g2[j] = (!a && poly_class(xh, yh, g2_threshold)) ? 1u : 0u;
@@ -290,6 +301,8 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
                                      const uint32_t* __restrict__ zpos,
                                      const uint32_t* __restrict__ flag_a,
                                      const uint32_t* __restrict__ scan_a,
+                                     const uint32_t* __restrict__ flag_a2,
+                                     const uint32_t* __restrict__ scan_a2,
                                      const uint32_t* __restrict__ flag_g2,
                                      const uint32_t* __restrict__ scan_g2,
                                      uint32_t* __restrict__ order, float4* __restrict__ qhl,
@@ -301,14 +314,15 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
     const size_t num_a = static_cast<size_t>(scan_a[q.n - 1]) + flag_a[q.n - 1];
     const size_t num_g2 = static_cast<size_t>(scan_g2[q.n - 1]) + flag_g2[q.n - 1];
     const size_t num_g1 = q.n - num_a - num_g2;
-    const bool is_a = flag_a[jz] != 0, is_g2 = flag_g2[jz] != 0;
+    const bool is_a = flag_a[jz] != 0, is_g2 = flag_g2[jz] != 0, is_a2 = flag_a2[jz] != 0;
     // General queries: 64-query blocks of G1 and G2 alternate, so a warp's
     // pair 0 (slots 0, 1) is G1 and pair 1 (slots 2, 3) is G2 — each warp
     // issues MUFU and FMA-pipe exponentials side by side.  Leftovers follow.
     // The general region comes first so its 128-query blocks align with warps.
     size_t i;
-    if (is_a) {
-        i = num_g1 + num_g2 + scan_a[jz];
+    if (is_a) {  // recipe region: alpha == 4 first, then alpha == 2
+        const size_t num_a2 = static_cast<size_t>(scan_a2[q.n - 1]) + flag_a2[q.n - 1];
+        i = num_g1 + num_g2 + (is_a2 ? (num_a - num_a2) + scan_a2[jz] : scan_a[jz] - scan_a2[jz]);
     } else {
         const size_t j = is_g2 ? scan_g2[jz] : jz - scan_a[jz] - scan_g2[jz];
         const size_t both = (num_g1 < num_g2 ? num_g1 : num_g2) / 64;  // full block pairs
@@ -334,11 +348,19 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
     // recipe path: w' = rcp((d2 s)^2), s = 1 or a power of two (exact)
     const bool snapped = q.snap_s[p] != kNoId;
     const double s = (snapped || d2n >= kRecipeLowD2) ? 1.0 : exp2(ceil(log2(kRecipeLowD2 / d2n)));
-    qpar[i] = make_float4(c, b, static_cast<float>(s), is_a ? 1.0f : (is_g2 ? 2.0f : 0.0f));
+    // recipe queries carry k1 in c: 1 for alpha == 4 (a = t^2), 0 for
+    // alpha == 2 (a = t); mixed warps pick per slot (recipe_a)
+    if (is_a) {
+        qpar[i] = make_float4(is_a2 ? 0.0f : 1.0f, is_a2 ? 1.0f : 0.0f,
+                              is_a2 ? 1.0f : static_cast<float>(s), is_a2 ? 3.0f : 1.0f);
+    } else {
+        qpar[i] = make_float4(c, b, static_cast<float>(s), is_g2 ? 2.0f : 0.0f);
+    }
     // log2(true weight) = log2(kernel weight) + shift (settle's overflow test)
     const double l2inv = log2(f.inv_scale);
-    lshift[i] = is_a ? 2.0 * log2(s) + 4.0 * l2inv
-                     : -static_cast<double>(b) - 2.0 * static_cast<double>(c) * l2inv;
+    lshift[i] = is_a2  ? 2.0 * l2inv
+              : is_a   ? 2.0 * log2(s) + 4.0 * l2inv
+                       : -static_cast<double>(b) - 2.0 * static_cast<double>(c) * l2inv;
     if (alpha == 4.0 && alpha4) atomicAdd(alpha4, 1ull);
 }
 
@@ -394,6 +416,17 @@ __device__ __forceinline__ f2 rcp2(f2 v) {
     float lo, hi;
     up2(v, lo, hi);
     return pk2(mufu_rcp(lo), mufu_rcp(hi));
+}
+
+// Mixed recipe warps (only the one warp straddling the alpha == 4 / alpha == 2
+// boundary of the recipe region): a = t^2 for an alpha == 4 slot (k1 = 1),
+// t for an alpha == 2 slot (k1 = 0), bit-identical to the pure modes; a
+// select, not t * fma(k1, t, k0), because padding records give t = inf.
+__device__ __forceinline__ f2 recipe_a(f2 t, f2 k1) {
+    float t0, t1, k0, kk1;
+    up2(t, t0, t1);
+    up2(k1, k0, kk1);
+    return pk2(k0 != 0.0f ? __fmul_rn(t0, t0) : t0, kk1 != 0.0f ? __fmul_rn(t1, t1) : t1);
 }
 
 // exp2 on the FMA pipe for class-G2 queries (x <= ~0 after ratio scaling):
@@ -531,9 +564,12 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
             const f2 d1 = add2(fma2(bc2(Y.y), fy[r], fma2(bc2(X.y), fx[r], fq[r])), bc2(P.y));
             const f2 d2 = add2(fma2(bc2(Y.z), fy[r], fma2(bc2(X.z), fx[r], fq[r])), bc2(P.z));
             const f2 d3 = add2(fma2(bc2(Y.w), fy[r], fma2(bc2(X.w), fx[r], fq[r])), bc2(P.w));
-            if (MODE == 3) {
-                const f2 a0 = mul2(d0, d0), a1 = mul2(d1, d1);
-                const f2 a2 = mul2(d2, d2), a3 = mul2(d3, d3);
+            if (MODE == 3 || MODE == 7 || MODE == 8) {
+                // a = d2^2 (alpha 4), d2 (alpha 2), a per-slot pick (mixed)
+                const f2 a0 = MODE == 3 ? mul2(d0, d0) : MODE == 7 ? d0 : recipe_a(d0, q.c[r]);
+                const f2 a1 = MODE == 3 ? mul2(d1, d1) : MODE == 7 ? d1 : recipe_a(d1, q.c[r]);
+                const f2 a2 = MODE == 3 ? mul2(d2, d2) : MODE == 7 ? d2 : recipe_a(d2, q.c[r]);
+                const f2 a3 = MODE == 3 ? mul2(d3, d3) : MODE == 7 ? d3 : recipe_a(d3, q.c[r]);
                 const f2 r01 = rcp2(mul2(a0, a1));
                 sw[r] = fma2(r01, add2(a0, a1), sw[r]);
                 swz[r] = fma2(r01, fma2(a1, bc2(Z.x), mul2(a0, bc2(Z.y))), swz[r]);
@@ -575,7 +611,8 @@ template <int MODE, int QT>
 __device__ __forceinline__ void k4_near_point(float pxh, float pyh, float pxl, float pyl,
                                               float pzh, float pzl, const QState<QT>& q,
                                               const QCoords (&qc)[QT / 2], f2 (&sw)[QT / 2],
-                                              f2 (&swz)[QT / 2], f2 (&cz)[QT / 2]) {
+                                              f2 (&swz)[QT / 2], f2 (&cz)[QT / 2],
+                                              f2 (&cw)[QT / 2]) {
     constexpr int kPairs = QT / 2;
 #pragma unroll
     for (int r = 0; r < kPairs; ++r) {
@@ -586,10 +623,24 @@ __device__ __forceinline__ void k4_near_point(float pxh, float pyh, float pxl, f
         if (MODE == 3 || MODE == 0) {
             if (MODE == 0) d2 = mul2(d2, q.s[r]);
             w = rcp2(mul2(d2, d2));
+        } else if (MODE == 7) {  // alpha == 2: s == 1
+            w = rcp2(d2);
+        } else if (MODE == 8) {  // mixed recipe: t = d2 s, a = t^2 or t per slot
+            d2 = mul2(d2, q.s[r]);
+            w = rcp2(recipe_a(d2, q.c[r]));
         } else {
             w = general_w<MODE, QT>(d2, q, r);
         }
+#if AIDW_K4_NEAR_KAHAN_SW
+        {
+            const f2 yw = sub2(w, cw[r]);
+            const f2 s1 = add2(sw[r], yw);
+            cw[r] = sub2(sub2(s1, sw[r]), yw);
+            sw[r] = s1;
+        }
+#else
         sw[r] = add2(sw[r], w);
+#endif
         const f2 tz = fma2(w, bc2(pzh), mul2(w, bc2(pzl)));
         const f2 y = sub2(tz, cz[r]);
         const f2 s2 = add2(swz[r], y);
@@ -601,7 +652,8 @@ __device__ __forceinline__ void k4_near_point(float pxh, float pyh, float pxl, f
 template <int MODE, int QT>
 __device__ __forceinline__ void k4_near(const float* __restrict__ t, const QState<QT>& q,
                                         const QCoords (&qc)[QT / 2], f2 (&sw)[QT / 2],
-                                        f2 (&swz)[QT / 2], f2 (&cz)[QT / 2]) {
+                                        f2 (&swz)[QT / 2], f2 (&cz)[QT / 2],
+                                        f2 (&cw)[QT / 2]) {
 #pragma unroll 1
     for (int j = 0; j < kWeightTile; j += 4) {
         const float4 X = *reinterpret_cast<const float4*>(t + kXH * kWeightTile + j);
@@ -610,10 +662,10 @@ __device__ __forceinline__ void k4_near(const float* __restrict__ t, const QStat
         const float4 YL = *reinterpret_cast<const float4*>(t + kYL * kWeightTile + j);
         const float4 Z = *reinterpret_cast<const float4*>(t + kZH * kWeightTile + j);
         const float4 ZL = *reinterpret_cast<const float4*>(t + kZL * kWeightTile + j);
-        k4_near_point<MODE, QT>(X.x, Y.x, XL.x, YL.x, Z.x, ZL.x, q, qc, sw, swz, cz);
-        k4_near_point<MODE, QT>(X.y, Y.y, XL.y, YL.y, Z.y, ZL.y, q, qc, sw, swz, cz);
-        k4_near_point<MODE, QT>(X.z, Y.z, XL.z, YL.z, Z.z, ZL.z, q, qc, sw, swz, cz);
-        k4_near_point<MODE, QT>(X.w, Y.w, XL.w, YL.w, Z.w, ZL.w, q, qc, sw, swz, cz);
+        k4_near_point<MODE, QT>(X.x, Y.x, XL.x, YL.x, Z.x, ZL.x, q, qc, sw, swz, cz, cw);
+        k4_near_point<MODE, QT>(X.y, Y.y, XL.y, YL.y, Z.y, ZL.y, q, qc, sw, swz, cz, cw);
+        k4_near_point<MODE, QT>(X.z, Y.z, XL.z, YL.z, Z.z, ZL.z, q, qc, sw, swz, cz, cw);
+        k4_near_point<MODE, QT>(X.w, Y.w, XL.w, YL.w, Z.w, ZL.w, q, qc, sw, swz, cz, cw);
     }
 }
 
@@ -643,14 +695,14 @@ __device__ __forceinline__ void k4_tile(const float* __restrict__ t, const QStat
         // far pairs never need the recipe's range scaling (d2 >= the near
         // threshold >= 1e-8): mode 0 runs the s-free form and rescales the
         // tile sums by s^-2 (a power of two: exact)
-        k4_far<MODE == 0 ? 3 : MODE, QT>(t, q, fx, fy, fq, sw, swz);
+        k4_far<MODE == 0 ? 3 : MODE, QT>(t, q, fx, fy, fq, sw, swz);  // 7, 8: s-free too
 #pragma unroll
         for (int r = 0; r < kPairs; ++r) {
             float w0, w1, z0, z1;
             up2(sw[r], w0, w1);
             up2(swz[r], z0, z1);
             double m0 = 1.0, m1 = 1.0;
-            if (MODE == 0) {
+            if (MODE == 0 || MODE == 8) {  // (alpha == 2 queries have s == 1)
                 float s0, s1;
                 up2(q.s[r], s0, s1);
                 m0 = 1.0 / (static_cast<double>(s0) * s0);
@@ -663,20 +715,25 @@ __device__ __forceinline__ void k4_tile(const float* __restrict__ t, const QStat
     if (any_near) {
         QCoords qc[kPairs];
         load_coords<QT>(qhl, wbase, lane, q1, qc);
-        f2 sw[kPairs], swz[kPairs], cz[kPairs];
+        f2 sw[kPairs], swz[kPairs], cz[kPairs], cw[kPairs];
 #pragma unroll
-        for (int r = 0; r < kPairs; ++r) sw[r] = swz[r] = cz[r] = 0ull;
-        k4_near<MODE, QT>(t, q, qc, sw, swz, cz);
+        for (int r = 0; r < kPairs; ++r) sw[r] = swz[r] = cz[r] = cw[r] = 0ull;
+        k4_near<MODE, QT>(t, q, qc, sw, swz, cz, cw);
 #pragma unroll
         for (int r = 0; r < kPairs; ++r) {
             float w0, w1, z0, z1, c0, c1;
             up2(sw[r], w0, w1);
             up2(swz[r], z0, z1);
             up2(cz[r], c0, c1);
+            float e0 = 0.0f, e1 = 0.0f;
+#if AIDW_K4_NEAR_KAHAN_SW
+            up2(cw[r], e0, e1);
+#endif
             if (nq[2 * r])
-                SW[2 * r] += w0, SWZ[2 * r] += static_cast<double>(z0) - static_cast<double>(c0);
+                SW[2 * r] += static_cast<double>(w0) - static_cast<double>(e0),
+                    SWZ[2 * r] += static_cast<double>(z0) - static_cast<double>(c0);
             if (nq[2 * r + 1])
-                SW[2 * r + 1] += w1,
+                SW[2 * r + 1] += static_cast<double>(w1) - static_cast<double>(e1),
                     SWZ[2 * r + 1] += static_cast<double>(z1) - static_cast<double>(c1);
         }
     }
@@ -700,7 +757,7 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t wbase = q0 + cta * (kK4Threads * kQT) + static_cast<size_t>(warp) * (32 * kQT);
     QState<kQT> q;
-    bool any_g1 = false, any_g2 = false, any_scaled = false;
+    bool any_g1 = false, any_g2 = false, any_scaled = false, any_r2 = false, any_r4 = false;
     {
         float4 r[kQT];
 #pragma unroll
@@ -710,6 +767,8 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
             q.v[i] = p < q1;
             if (q.v[i]) r[i] = a.qpar[p];
             q.g2[i] = r[i].w == 2.0f;
+            any_r2 |= q.v[i] && r[i].w == 3.0f;
+            any_r4 |= q.v[i] && r[i].w == 1.0f;
             any_g2 |= q.v[i] && q.g2[i];
             any_g1 |= q.v[i] && !q.g2[i];
             any_scaled |= q.v[i] && r[i].z != 1.0f;
@@ -725,9 +784,14 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
     any_g1 = __any_sync(0xFFFFFFFFu, any_g1);
     any_g2 = __any_sync(0xFFFFFFFFu, any_g2);
     any_scaled = __any_sync(0xFFFFFFFFu, any_scaled);
+    any_r2 = __any_sync(0xFFFFFFFFu, any_r2);
+    any_r4 = __any_sync(0xFFFFFFFFu, any_r4);
     int mode;
     if (RECIPE) {
-        mode = any_scaled ? 0 : 3;
+        mode = any_r2 ? (any_r4 ? 8 : 7) : (any_scaled ? 0 : 3);
+#ifdef AIDW_K4_FORCE_MIXED
+        mode = 8;
+#endif
     } else {
         // the interleaved layout: pair 0 all G1 and pair 1 all G2 across the warp
         bool split = kQT == 4;
@@ -774,6 +838,8 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
         any_far = __any_sync(0xFFFFFFFFu, any_far);
         if (RECIPE) {
             if (mode == 3) k4_tile<3, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
+            else if (mode == 7) k4_tile<7, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
+            else if (mode == 8) k4_tile<8, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
             else k4_tile<0, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
         } else {
             if (mode == 5) k4_tile<5, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
@@ -936,7 +1002,8 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
            sp.tiles, rfar * rfar, diagf * diagf, tbox.get(), tgeo.get());
     border.release();
 
-    DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), flag_g2(q.n, s), scan_g2(q.n, s), order_q(q.n, s);
+    DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), flag_g2(q.n, s), scan_g2(q.n, s), order_q(q.n, s),
+        flag_a2(q.n, s), scan_a2(q.n, s);
     DBuf<float4> qhl(q.n, s), qpar(q.n, s);
     DBuf<double> lshift(q.n, s);
     DBuf<uint32_t> zkey(q.n, s), zpos(q.n, s);
@@ -952,12 +1019,13 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
         return static_cast<unsigned>(std::fmin(share, 1.0) * 4294967295.0);
     }();
     LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f,
-           g_alpha4_recipe.load() ? 1 : 0, g2_threshold, zpos.get(), flag.get(), flag_g2.get());
+           g_alpha4_recipe.load() ? 1 : 0, g2_threshold, zpos.get(), flag.get(), flag_a2.get(),
+           flag_g2.get());
     exclusive_scan_u32(flag.get(), scan_a.get(), q.n, s);
+    exclusive_scan_u32(flag_a2.get(), scan_a2.get(), q.n, s);
     exclusive_scan_u32(flag_g2.get(), scan_g2.get(), q.n, s);
     LAUNCH(query_records_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, zpos.get(),
-           flag.get(),
-           scan_a.get(), flag_g2.get(), scan_g2.get(), order_q.get(), qhl.get(), qpar.get(),
+           flag.get(), scan_a.get(), flag_a2.get(), scan_a2.get(), flag_g2.get(), scan_g2.get(), order_q.get(), qhl.get(), qpar.get(),
            lshift.get(), times ? times->d_alpha4 : nullptr);
 
     DBuf<double2> part(q.n * sp.chunks, s);

@@ -96,6 +96,22 @@ def test_idw_mode_vs_oracle(alpha):
     assert np.all(out.result.alphas == alpha) and out.k_effective == 0
 
 
+@pytest.mark.parametrize("scale", [1.0, 1e-3])
+def test_mixed_recipe_classes_alpha2_alpha4(scale):
+    # levels saturating at exactly 2 and 4 on clustered data: warps mix the
+    # w = 1/d^2 and w = 1/d^4 recipe classes with general-alpha queries; a
+    # small domain exercises the per-query ratio scaling (s != 1) of alpha 4
+    xs, ys, zs = O.generate_clustered(30_000, seed=11)
+    xs, ys = xs * scale, ys * scale
+    qx, qy = O.generate_queries(3000, (0.0, 0.0, scale, scale), 12)
+    p = A.AidwParams(k=10, alpha_levels=(2.0, 2.0, 3.0, 4.0, 4.0))
+    out = A.run_pipeline(A.PointSet(xs, ys, zs), A.PointSet(qx, qy), A.RunConfig(params=p))
+    ref = O.pipeline(xs, ys, zs, qx, qy, k=10, variant=1, levels=p.alpha_levels)
+    assert np.max(np.abs(out.result.alphas - ref["alpha"]) / ref["alpha"]) <= 1e-12
+    assert np.any(out.result.alphas == 2.0) and np.any(out.result.alphas == 4.0)
+    assert pred_err(out.result.predicted, ref["pred"], zs) <= 1e-5
+
+
 def test_tiny_sizes():
     # m = 1: every prediction is the single value
     one = A.PointSet([0.3], [0.4], [42.0])
