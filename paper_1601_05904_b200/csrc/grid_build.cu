@@ -6,10 +6,11 @@
 //   1. cell_ids_kernel  : FP64 locate_cell per point (exact reference
 //                         rounding), key = row-major cell id, value = index,
 //                         per-cell histogram with global atomics;
-//   2. exclusive_scan   : cell_start = exclusive prefix of the histogram;
+//   2. exclusive_scan   : cell_start = exclusive prefix of the histogram
+//                         (single pass, decoupled look-back);
 //   3. counting sort    : scatter through per-cell atomic cursors, then each
-//                         cell's ids sorted ascending (thread per cell of <= 16
-//                         points, warp rank placement up to 256, CTA bitonic up
+//                         cell's ids sorted ascending (thread per point: rank in
+//                         its cell of <= 16 points; warp rank placement up to 256, CTA bitonic up
 //                         to 4096, stable compaction beyond) fused with the gather of the cell-sorted
 //                         x / y.  (radix_sort_pairs — stable LSD, 8-bit digits,
 //                         warp __match_any ranking — sorts the queries by cell.)
@@ -52,7 +53,7 @@ __global__ void cell_ids_kernel(const double* __restrict__ x, const double* __re
         atomicMin(fail, static_cast<long long>(i));
     }
     keys[i] = cell;
-    vals[i] = static_cast<uint32_t>(i);
+    if (vals) vals[i] = static_cast<uint32_t>(i);
 }
 
 __global__ void interleave_kernel(const double* __restrict__ x, const double* __restrict__ y,
@@ -72,44 +73,87 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v) {
     return v;
 }
 
-// Block-local exclusive scan of a 2048-value tile; tile totals -> sums.
-__global__ void scan_tiles_kernel(const uint32_t* in, uint32_t* out, size_t n,
-                                  uint32_t* __restrict__ sums) {
-    __shared__ uint32_t warp_total[kThreads / 32];
-    const size_t base = static_cast<size_t>(blockIdx.x) * kScanTile +
-                        static_cast<size_t>(threadIdx.x) * kScanItems;
+// Single-pass exclusive scan (decoupled look-back): tiles of 2048 values are
+// taken in ticket order; each warp scans 256 values (row-strided: element
+// j * 32 + lane of its segment, so loads and stores are coalesced), the tile
+// publishes its aggregate, then lane 0 of warp 0 walks back over the
+// predecessors' (flag, value) words until an inclusive prefix is found.
+// In place (in == out) is allowed: a tile reads all its values first.
+constexpr unsigned long long kScanAggregate = 1ull << 32, kScanPrefix = 2ull << 32;
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) scan_onepass_kernel(
+    const uint32_t* in, uint32_t* out, size_t n, unsigned long long* __restrict__ status,
+    unsigned* __restrict__ ticket) {
+    __shared__ unsigned s_tile;
+    __shared__ uint32_t s_warp[kThreads / 32];
+    __shared__ uint32_t s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t base = static_cast<size_t>(tile) * kScanTile + static_cast<size_t>(warp) * 32 * kScanItems;
     uint32_t v[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const size_t idx = base + static_cast<size_t>(j) * 32 + lane;
+        v[j] = idx < n ? in[idx] : 0u;
+    }
     uint32_t run = 0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        const size_t idx = base + j;
-        v[j] = idx < n ? in[idx] : 0u;
-        run += v[j];
+        const uint32_t inc = warp_inclusive_scan(v[j]);
+        const uint32_t x = v[j];
+        v[j] = run + inc - x;  // exclusive within the warp's segment
+        run += __shfl_sync(0xFFFFFFFFu, inc, 31);
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t incl = warp_inclusive_scan(run);
-    if (lane == 31) warp_total[warp] = incl;
+    if (lane == 0) s_warp[warp] = run;
     __syncthreads();
     if (warp == 0) {
-        uint32_t t = lane < kThreads / 32 ? warp_total[lane] : 0u;
-        t = warp_inclusive_scan(t);
-        if (lane < kThreads / 32) warp_total[lane] = t;
+        const uint32_t t = lane < kThreads / 32 ? s_warp[lane] : 0u;
+        const uint32_t inc = warp_inclusive_scan(t);
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, kThreads / 32 - 1);
+        if (lane < kThreads / 32) s_warp[lane] = inc - t;
+        // warp-wide look-back: lane l inspects tile (j - l) of a 32-tile
+        // window; the window's aggregates are summed down to the nearest
+        // inclusive prefix (tile -1 counts as an inclusive prefix of 0)
+        if (lane == 0)
+            st_release(&status[tile], (tile == 0 ? kScanPrefix : kScanAggregate) | total);
+        uint32_t prefix = 0;
+        for (long long jbase = static_cast<long long>(tile) - 1;;) {
+            const long long jj = jbase - lane;
+            const unsigned long long w = jj >= 0 ? ld_acquire(&status[jj]) : kScanPrefix;
+            const unsigned pmask = __ballot_sync(0xFFFFFFFFu, (w & kScanPrefix) != 0);
+            const int stop = pmask ? __ffs(pmask) - 1 : 31;
+            // a tile up to the nearest prefix not published yet: look again
+            if (__any_sync(0xFFFFFFFFu, lane <= stop && (w >> 32) == 0)) continue;
+            uint32_t val = lane <= stop ? static_cast<uint32_t>(w) : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, o);
+            prefix += val;
+            if (pmask) break;
+            jbase -= 32;
+        }
+        if (lane == 0) {
+            if (tile != 0) st_release(&status[tile], kScanPrefix | static_cast<uint32_t>(prefix + total));
+            s_prefix = prefix;
+        }
     }
     __syncthreads();
-    uint32_t prefix = incl - run + (warp > 0 ? warp_total[warp - 1] : 0u);
+    const uint32_t add = s_prefix + s_warp[warp];
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        const size_t idx = base + j;
-        if (idx < n) out[idx] = prefix;
-        prefix += v[j];
+        const size_t idx = base + static_cast<size_t>(j) * 32 + lane;
+        if (idx < n) out[idx] = v[j] + add;
     }
-    if (threadIdx.x == kThreads - 1 && sums) sums[blockIdx.x] = prefix;
-}
-
-__global__ void add_tile_offsets_kernel(uint32_t* out, size_t n,
-                                        const uint32_t* __restrict__ offsets) {
-    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) out[i] += offsets[i / kScanTile];
 }
 
 // ---------------------------------------------------------------- radix sort
@@ -246,7 +290,24 @@ __global__ void minmax_kernel(const double* __restrict__ ax, const double* __res
         lo[q] = warp_min_u64(lo[q]);
         hi[q] = warp_max_u64(hi[q]);
     }
-    if ((threadIdx.x & 31) == 0) {
+    // CTA reduction first: one atomic per key per CTA (per-warp atomics on
+    // the same six words serialise in L2)
+    __shared__ unsigned long long s_k[6][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) s_k[q][warp] = lo[q], s_k[3 + q][warp] = hi[q];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = static_cast<int>(blockDim.x >> 5);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            lo[q] = warp_min_u64(lane < nw ? s_k[q][lane] : ~0ull);
+            hi[q] = warp_max_u64(lane < nw ? s_k[3 + q][lane] : 0ull);
+        }
+    }
+    if (threadIdx.x == 0) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             atomicMin(&keys[q], lo[q]);
@@ -272,9 +333,9 @@ __global__ void decode_minmax_kernel(const unsigned long long* __restrict__ keys
 // too): histogram (cell_ids_kernel) -> exclusive scan (cell_start) ->
 // scatter through per-cell atomic cursors (order within a cell arbitrary) ->
 // each cell's ids sorted ascending, which is exactly the reference's stable
-// order, fused with the coordinate gather.  Cells of <= kSmallCell points
-// are sorted by one thread each, up to kMidCell by a warp, larger ones by a
-// CTA (cell_sort_big_kernel).
+// order, fused with the coordinate gather.  Points of cells of <= kSmallCell
+// points are placed by one thread each (rank among the cell's ids), cells up
+// to kMidCell by a warp, larger ones by a CTA (cell_sort_big_kernel).
 constexpr int kSmallCell = 16;
 constexpr int kMidCell = 256;
 constexpr int kBigCell = 4096;
@@ -298,36 +359,34 @@ __device__ __forceinline__ void emit_point(size_t s, uint32_t id, const double* 
     }
 }
 
-// One thread per cell of <= kSmallCell points: insertion sort in registers /
-// L1, then the gather.  Larger cells are queued for cell_sort_big_kernel.
-__global__ void cell_sort_small_kernel(const uint32_t* __restrict__ cell_start, size_t cells,
+// One thread per scattered position: a point of a cell of <= kSmallCell
+// points is placed by its rank among the cell's ids (ids are distinct, so the
+// ascending order is the reference's stable order), fused with the gather.
+// The first position of a larger cell queues it for the warp / CTA kernels.
+__global__ void cell_rank_small_kernel(const uint32_t* __restrict__ cell_start,
+                                       const uint32_t* __restrict__ keys, size_t m,
                                        const uint32_t* __restrict__ scattered,
                                        const double* __restrict__ x, const double* __restrict__ y,
                                        uint32_t* __restrict__ ids, double2* __restrict__ sxy,
                                        double* __restrict__ sx, double* __restrict__ sy,
                                        uint32_t* __restrict__ mid, uint32_t* __restrict__ big,
                                        uint32_t* __restrict__ nbig) {
-    const size_t c = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= cells) return;
+    const size_t p = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    const uint32_t id = scattered[p];
+    const uint32_t c = keys[id];
     const uint32_t b = cell_start[c], e = cell_start[c + 1];
     const uint32_t n = e - b;
-    if (n == 0) return;
     if (n > kSmallCell) {  // nbig[0]: warp-sized cells, nbig[1]: CTA-sized
-        if (n <= kMidCell) mid[atomicAdd(&nbig[0], 1u)] = static_cast<uint32_t>(c);
-        else big[atomicAdd(&nbig[1], 1u)] = static_cast<uint32_t>(c);
+        if (p == b) {
+            if (n <= kMidCell) mid[atomicAdd(&nbig[0], 1u)] = c;
+            else big[atomicAdd(&nbig[1], 1u)] = c;
+        }
         return;
     }
-    uint32_t v[kSmallCell];
-    for (uint32_t j = 0; j < n; ++j) {
-        const uint32_t t = scattered[b + j];
-        uint32_t k = j;
-        while (k > 0 && v[k - 1] > t) {
-            v[k] = v[k - 1];
-            --k;
-        }
-        v[k] = t;
-    }
-    for (uint32_t j = 0; j < n; ++j) emit_point(b + j, v[j], x, y, ids, sxy, sx, sy);
+    uint32_t rank = 0;
+    for (uint32_t q = b; q < e; ++q) rank += scattered[q] < id ? 1u : 0u;
+    emit_point(b + rank, id, x, y, ids, sxy, sx, sy);
 }
 
 // One warp per queued cell of kSmallCell < n <= kMidCell points: the ids go
@@ -470,14 +529,11 @@ int bits_for(uint64_t max_key) {
 void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, size_t n, cudaStream_t s) {
     if (n == 0) return;
     const unsigned tiles = ceil_div(n, kScanTile);
-    if (tiles == 1) {
-        LAUNCH(scan_tiles_kernel, 1, kThreads, 0, s, d_in, d_out, n, nullptr);
-        return;
-    }
-    DBuf<uint32_t> sums(tiles, s);
-    LAUNCH(scan_tiles_kernel, tiles, kThreads, 0, s, d_in, d_out, n, sums.get());
-    exclusive_scan_u32(sums.get(), sums.get(), tiles, s);
-    LAUNCH(add_tile_offsets_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_out, n, sums.get());
+    // status words (one per tile) + the tile ticket, zeroed together
+    DBuf<unsigned long long> status(static_cast<size_t>(tiles) + 1, s);
+    CK(cudaMemsetAsync(status.get(), 0, (static_cast<size_t>(tiles) + 1) * sizeof(unsigned long long), s));
+    LAUNCH(scan_onepass_kernel, tiles, kThreads, 0, s, d_in, d_out, n, status.get(),
+           reinterpret_cast<unsigned*>(status.get() + tiles));
 }
 
 void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaStream_t s) {
@@ -540,15 +596,15 @@ void build_grid_device(const double* d_x, const double* d_y, size_t m,
     CK(cudaMemsetAsync(out.cell_start.get(), 0, (cells + 1) * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(nbig.get(), 0, 2 * sizeof(uint32_t), s));
     LAUNCH(cell_ids_kernel, ceil_div(m, kThreads), kThreads, 0, s, d_x, d_y, m, g, keys.get(),
-           vals.get(), out.cell_start.get(), d_fail);
+           static_cast<uint32_t*>(nullptr), out.cell_start.get(), d_fail);
     exclusive_scan_u32(out.cell_start.get(), out.cell_start.get(), cells + 1, s);
     // counting sort: cursors start at cell_start; vals receives the scatter
     CK(cudaMemcpyAsync(cursor.get(), out.cell_start.get(), cells * sizeof(uint32_t),
                        cudaMemcpyDeviceToDevice, s));
     LAUNCH(cell_scatter_kernel, ceil_div(m, kThreads), kThreads, 0, s, keys.get(), m,
            cursor.get(), vals.get());
-    LAUNCH(cell_sort_small_kernel, ceil_div(cells, kThreads), kThreads, 0, s,
-           out.cell_start.get(), cells, vals.get(), d_x, d_y, out.sorted_ids.get(),
+    LAUNCH(cell_rank_small_kernel, ceil_div(m, kThreads), kThreads, 0, s,
+           out.cell_start.get(), keys.get(), m, vals.get(), d_x, d_y, out.sorted_ids.get(),
            out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get(), mid.get(), big.get(),
            nbig.get());
     LAUNCH(cell_sort_mid_kernel, 148u * 4u, 256, 0, s, out.cell_start.get(), mid.get(),

@@ -54,6 +54,12 @@ namespace {
 #define AIDW_K4_MINB 2
 #endif
 constexpr int kK4Threads = AIDW_K4_THREADS;
+#ifndef AIDW_K4_ALLPAIRS
+#define AIDW_K4_ALLPAIRS 0
+#endif
+#ifndef AIDW_K4_MIXPAIRS
+#define AIDW_K4_MIXPAIRS 0
+#endif
 #ifndef AIDW_K4_NEAR_KAHAN_SW
 #define AIDW_K4_NEAR_KAHAN_SW 1
 #endif
@@ -552,8 +558,13 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
                                        const f2 (&fq)[QT / 2], f2 (&sw)[QT / 2],
                                        f2 (&swz)[QT / 2]) {
     constexpr int kPairs = QT / 2;
-#pragma unroll kFarUnroll
-    for (int j = 0; j < kWeightTile; j += 4) {
+#pragma unroll 1
+    for (int j0 = 0; j0 < kWeightTile; j0 += 4 * kFarUnroll) {
+#pragma unroll
+    for (int h = 0; h < kFarUnroll; ++h) {
+        const int j = j0 + 4 * h;
+        // points 2, 3 of the group paired too (AIDW_K4_MIXPAIRS: every other group)
+        const bool pair23 = AIDW_K4_ALLPAIRS || (AIDW_K4_MIXPAIRS && h == 0);
         const float4 X = *reinterpret_cast<const float4*>(t + kPX * kWeightTile + j);
         const float4 Y = *reinterpret_cast<const float4*>(t + kPY * kWeightTile + j);
         const float4 P = *reinterpret_cast<const float4*>(t + kPP * kWeightTile + j);
@@ -573,18 +584,18 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
                 const f2 r01 = rcp2(mul2(a0, a1));
                 sw[r] = fma2(r01, add2(a0, a1), sw[r]);
                 swz[r] = fma2(r01, fma2(a1, bc2(Z.x), mul2(a0, bc2(Z.y))), swz[r]);
-#if AIDW_K4_ALLPAIRS
-                const f2 r23 = rcp2(mul2(a2, a3));
-                sw[r] = fma2(r23, add2(a2, a3), sw[r]);
-                swz[r] = fma2(r23, fma2(a3, bc2(Z.z), mul2(a2, bc2(Z.w))), swz[r]);
-#else
-                const f2 w2 = rcp2(a2);
-                sw[r] = add2(sw[r], w2);
-                swz[r] = fma2(w2, bc2(Z.z), swz[r]);
-                const f2 w3 = rcp2(a3);
-                sw[r] = add2(sw[r], w3);
-                swz[r] = fma2(w3, bc2(Z.w), swz[r]);
-#endif
+                if (pair23) {
+                    const f2 r23 = rcp2(mul2(a2, a3));
+                    sw[r] = fma2(r23, add2(a2, a3), sw[r]);
+                    swz[r] = fma2(r23, fma2(a3, bc2(Z.z), mul2(a2, bc2(Z.w))), swz[r]);
+                } else {
+                    const f2 w2 = rcp2(a2);
+                    sw[r] = add2(sw[r], w2);
+                    swz[r] = fma2(w2, bc2(Z.z), swz[r]);
+                    const f2 w3 = rcp2(a3);
+                    sw[r] = add2(sw[r], w3);
+                    swz[r] = fma2(w3, bc2(Z.w), swz[r]);
+                }
             } else {
                 const f2 w0 = general_w<MODE, QT>(d0, q, r);
                 sw[r] = add2(sw[r], w0);
@@ -600,6 +611,7 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
                 swz[r] = fma2(w3, bc2(Z.w), swz[r]);
             }
         }
+    }
     }
 }
 
