@@ -170,9 +170,10 @@ __global__ void prep_data_kernel(const double* __restrict__ x, const double* __r
 
 // One warp per tile: bounding box of the real records (hi parts), centre c,
 // near threshold, and the far-form components.  A (query, tile) pair is FAR
-// when the query's distance to the box exceeds both R_far and the box
-// diagonal: then |q'| + |p'| <= 2 d, so the expanded d2 loses at most a few
-// ulp of d2 (~1e-7 relative), against ~1e-6 for plain hi differences.
+// when the query's distance d to the box exceeds both R_far and 0.3 box
+// diagonals: then |q'| + |p'| <= d + diag <= 4.4 d, so the expanded d2 loses
+// at most a few ulp of 19 d2 (the measured contract error is unchanged from
+// a 0.5-diagonal rule: tools/accuracy sweeps in DESIGN.md).
 // Partial (padded) tiles are always NEAR.
 __global__ void tile_geo_kernel(float* __restrict__ rec, size_t m, size_t tiles, float rfar2,
                                 float diagf2, float4* __restrict__ box, float4* __restrict__ geo) {
@@ -1008,7 +1009,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     // far form needs box distance >= diagf * tile diagonal (AIDW_K4_DIAGF)
     static const float diagf = [] {
         const char* v = std::getenv("AIDW_K4_DIAGF");
-        return v ? static_cast<float>(std::atof(v)) : 0.5f;
+        return v ? static_cast<float>(std::atof(v)) : 0.3f;
     }();
     LAUNCH(tile_geo_kernel, ceil_div(sp.tiles * 32, kThreads), kThreads, 0, s, rec.get(), d.m,
            sp.tiles, rfar * rfar, diagf * diagf, tbox.get(), tgeo.get());
