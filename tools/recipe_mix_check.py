@@ -1,3 +1,9 @@
+"""Recipe-class mixing check (GPU box): AIDW with alpha levels saturating at
+exactly 2 and 4 on clustered data, so warps of the alpha = 4 / alpha = 2
+recipe regions and the general region meet; prints the worst contract errors
+against the C oracle.  Run it against a library built with
+-DAIDW_K4_FORCE_MIXED=1 (tools/build_variant.sh, AIDW_LIB_PATH) to force
+every recipe warp through the per-slot mixed form — the errors must not move."""
 import sys; sys.path.insert(0,'.')
 import numpy as np, oracle as O, paper_1601_05904_b200 as A
 def pe(got, ref, zs):
