@@ -279,9 +279,18 @@ __global__ void morton_keys_kernel(const WeightQueries q, WeightFrame f, uint32_
 }
 
 // Flags by Morton rank j (p = zpos[j]).
+// Recipe sub-classes after alpha = 4 (region order): alpha = 2, 1, 3, and
+// the class codes the records carry (qpar.x and .w; general classes: 0, 2).
+constexpr int kRecipeSubs = 3;
+constexpr float kCodeA4 = 1.0f, kCodeA2 = 3.0f, kCodeA1 = 4.0f, kCodeA3 = 5.0f;
+struct RecipeFlags {
+    uint32_t* flag[kRecipeSubs];
+    uint32_t* scan[kRecipeSubs];
+};
+
 __global__ void class_flags_kernel(const WeightQueries q, WeightFrame f, int recipe,
                                    unsigned g2_threshold, const uint32_t* __restrict__ zpos,
-                                   uint32_t* __restrict__ flag_a, uint32_t* __restrict__ flag_a2,
+                                   uint32_t* __restrict__ flag_a, RecipeFlags rf,
                                    uint32_t* __restrict__ flag_g2) {
     const size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= q.n) return;
@@ -289,14 +298,16 @@ __global__ void class_flags_kernel(const WeightQueries q, WeightFrame f, int rec
     const double d2n = q.d2min_s[p] * f.inv_scale * f.inv_scale;
     const bool snapped = q.snap_s[p] != kNoId;
     const double alpha = q.alpha_s[p];
-    // recipe classes: alpha == 4 (w = 1 / d^4) and alpha == 2 (w = 1 / d^2;
-    // the reference's default IDW exponent), both half-integer recipes
-    // (interpolate.hpp:174-209)
-    const bool a2 = recipe && !snapped && alpha == 2.0 && d2n >= kRecipeMinD2;
-    const bool a = (recipe && alpha == 4.0 && d2n >= kRecipeMinD2) || snapped || a2;
+    // recipe classes — integer alpha among the reference's half-integer
+    // recipes (interpolate.hpp:174-209): alpha = 4 (w = 1/d^4; also every
+    // snapped query), 2 (1/d^2, the reference's default IDW exponent), 1 and 3
+    const bool ok = recipe && !snapped && d2n >= kRecipeMinD2;
+    const bool sub[kRecipeSubs] = {ok && alpha == 2.0, ok && alpha == 1.0, ok && alpha == 3.0};
+    const bool a = (ok && alpha == 4.0) || snapped || sub[0] || sub[1] || sub[2];
     const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
     flag_a[j] = a ? 1u : 0u;
-    flag_a2[j] = a2 ? 1u : 0u;
+#pragma unroll
+    for (int k = 0; k < kRecipeSubs; ++k) rf.flag[k][j] = sub[k] ? 1u : 0u;
     const float xh = __double2float_rn((q.qx[qi] - f.ox) * f.inv_scale);
     const float yh = __double2float_rn((q.qy[qi] - f.oy) * f.inv_scale);
     flag_g2[j] = (!a && poly_class(xh, yh, g2_threshold)) ? 1u : 0u;
@@ -308,8 +319,7 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
                                      const uint32_t* __restrict__ zpos,
                                      const uint32_t* __restrict__ flag_a,
                                      const uint32_t* __restrict__ scan_a,
-                                     const uint32_t* __restrict__ flag_a2,
-                                     const uint32_t* __restrict__ scan_a2,
+                                     const RecipeFlags rf,
                                      const uint32_t* __restrict__ flag_g2,
                                      const uint32_t* __restrict__ scan_g2,
                                      uint32_t* __restrict__ order, float4* __restrict__ qhl,
@@ -321,15 +331,29 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
     const size_t num_a = static_cast<size_t>(scan_a[q.n - 1]) + flag_a[q.n - 1];
     const size_t num_g2 = static_cast<size_t>(scan_g2[q.n - 1]) + flag_g2[q.n - 1];
     const size_t num_g1 = q.n - num_a - num_g2;
-    const bool is_a = flag_a[jz] != 0, is_g2 = flag_g2[jz] != 0, is_a2 = flag_a2[jz] != 0;
+    const bool is_a = flag_a[jz] != 0, is_g2 = flag_g2[jz] != 0;
+    int sub = -1;  // recipe sub-class (-1: alpha = 4)
     // General queries: 64-query blocks of G1 and G2 alternate, so a warp's
     // pair 0 (slots 0, 1) is G1 and pair 1 (slots 2, 3) is G2 — each warp
     // issues MUFU and FMA-pipe exponentials side by side.  Leftovers follow.
     // The general region comes first so its 128-query blocks align with warps.
     size_t i;
-    if (is_a) {  // recipe region: alpha == 4 first, then alpha == 2
-        const size_t num_a2 = static_cast<size_t>(scan_a2[q.n - 1]) + flag_a2[q.n - 1];
-        i = num_g1 + num_g2 + (is_a2 ? (num_a - num_a2) + scan_a2[jz] : scan_a[jz] - scan_a2[jz]);
+    if (is_a) {  // recipe region: alpha = 4 first, then alpha = 2, 1, 3
+        size_t cnt[kRecipeSubs], before = 0, total = 0;
+#pragma unroll
+        for (int k = 0; k < kRecipeSubs; ++k) {
+            cnt[k] = static_cast<size_t>(rf.scan[k][q.n - 1]) + rf.flag[k][q.n - 1];
+            total += cnt[k];
+            before += rf.scan[k][jz];
+            if (rf.flag[k][jz]) sub = k;
+        }
+        size_t off = num_a - total;  // alpha = 4 count
+        if (sub < 0) {
+            i = num_g1 + num_g2 + (scan_a[jz] - before);
+        } else {
+            for (int k = 0; k < sub; ++k) off += cnt[k];
+            i = num_g1 + num_g2 + off + rf.scan[sub][jz];
+        }
     } else {
         const size_t j = is_g2 ? scan_g2[jz] : jz - scan_a[jz] - scan_g2[jz];
         const size_t both = (num_g1 < num_g2 ? num_g1 : num_g2) / 64;  // full block pairs
@@ -355,19 +379,20 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
     // recipe path: w' = rcp((d2 s)^2), s = 1 or a power of two (exact)
     const bool snapped = q.snap_s[p] != kNoId;
     const double s = (snapped || d2n >= kRecipeLowD2) ? 1.0 : exp2(ceil(log2(kRecipeLowD2 / d2n)));
-    // recipe queries carry k1 in c: 1 for alpha == 4 (a = t^2), 0 for
-    // alpha == 2 (a = t); mixed warps pick per slot (recipe_a)
+    // recipe queries carry their class code in x and w (recipe_a / recipe_rsq)
     if (is_a) {
-        qpar[i] = make_float4(is_a2 ? 0.0f : 1.0f, is_a2 ? 1.0f : 0.0f,
-                              is_a2 ? 1.0f : static_cast<float>(s), is_a2 ? 3.0f : 1.0f);
+        const float code = sub == 0 ? kCodeA2 : sub == 1 ? kCodeA1 : sub == 2 ? kCodeA3 : kCodeA4;
+        qpar[i] = make_float4(code, 0.0f, sub < 0 ? static_cast<float>(s) : 1.0f, code);
     } else {
         qpar[i] = make_float4(c, b, static_cast<float>(s), is_g2 ? 2.0f : 0.0f);
     }
     // log2(true weight) = log2(kernel weight) + shift (settle's overflow test)
     const double l2inv = log2(f.inv_scale);
-    lshift[i] = is_a2  ? 2.0 * l2inv
-              : is_a   ? 2.0 * log2(s) + 4.0 * l2inv
-                       : -static_cast<double>(b) - 2.0 * static_cast<double>(c) * l2inv;
+    // (recipe weights are the true ones scaled by inv_scale^alpha, alpha = 4
+    // also by s^2)
+    lshift[i] = !is_a    ? -static_cast<double>(b) - 2.0 * static_cast<double>(c) * l2inv
+              : sub < 0  ? 2.0 * log2(s) + 4.0 * l2inv
+                         : alpha * l2inv;
     if (alpha == 4.0 && alpha4) atomicAdd(alpha4, 1ull);
 }
 
@@ -425,15 +450,46 @@ __device__ __forceinline__ f2 rcp2(f2 v) {
     return pk2(mufu_rcp(lo), mufu_rcp(hi));
 }
 
-// Mixed recipe warps (only the one warp straddling the alpha == 4 / alpha == 2
-// boundary of the recipe region): a = t^2 for an alpha == 4 slot (k1 = 1),
-// t for an alpha == 2 slot (k1 = 0), bit-identical to the pure modes; a
-// select, not t * fma(k1, t, k0), because padding records give t = inf.
-__device__ __forceinline__ f2 recipe_a(f2 t, f2 k1) {
-    float t0, t1, k0, kk1;
+__device__ __forceinline__ float mufu_rsq(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ f2 rsq2(f2 v) {
+    float lo, hi;
+    up2(v, lo, hi);
+    return pk2(mufu_rsq(lo), mufu_rsq(hi));
+}
+
+// Recipe classes (qpar.x / qpar.w code): 1 alpha = 4 (w = 1/t^2, paired
+// reciprocals), 3 alpha = 2 (w = 1/t, paired), 4 alpha = 1 (w = rsqrt t),
+// 5 alpha = 3 (w = (rsqrt t)^3).  Mixed warps (only those straddling a class
+// boundary of the recipe region) evaluate every form and pick per slot, with
+// the same roundings as the pure modes, so a query's result never depends
+// on its warp-mates.  Selects, not arithmetic blends: padding gives t = inf.
+__device__ __forceinline__ bool paired_code(float c) { return c == kCodeA4 || c == kCodeA2; }
+__device__ __forceinline__ f2 recipe_a(f2 t, f2 code) {  // paired classes: t^2 or t
+    float t0, t1, c0, c1;
     up2(t, t0, t1);
-    up2(k1, k0, kk1);
-    return pk2(k0 != 0.0f ? __fmul_rn(t0, t0) : t0, kk1 != 0.0f ? __fmul_rn(t1, t1) : t1);
+    up2(code, c0, c1);
+    return pk2(c0 == kCodeA4 ? __fmul_rn(t0, t0) : t0, c1 == kCodeA4 ? __fmul_rn(t1, t1) : t1);
+}
+__device__ __forceinline__ f2 cube2(f2 r) { return mul2(mul2(r, r), r); }
+__device__ __forceinline__ f2 recipe_rsq(f2 t, f2 code) {  // rsqrt classes: r or r^3
+    const f2 r = rsq2(t);
+    const f2 r3 = cube2(r);
+    float a0, a1, b0, b1, c0, c1;
+    up2(r, a0, a1);
+    up2(r3, b0, b1);
+    up2(code, c0, c1);
+    return pk2(c0 == kCodeA3 ? b0 : a0, c1 == kCodeA3 ? b1 : a1);
+}
+__device__ __forceinline__ f2 sel_paired(f2 code, f2 x, f2 y) {
+    float x0, x1, y0, y1, c0, c1;
+    up2(x, x0, x1);
+    up2(y, y0, y1);
+    up2(code, c0, c1);
+    return pk2(paired_code(c0) ? x0 : y0, paired_code(c1) ? x1 : y1);
 }
 
 // exp2 on the FMA pipe for class-G2 queries (x <= ~0 after ratio scaling):
@@ -528,8 +584,11 @@ __device__ __forceinline__ void load_coords(const float4* qhl, size_t wbase, int
 //   4  general, all G2                        ex2 on the FMA pipe      (1 MUFU)
 //   5  general, pair 0 G1 / pair 1 G2 (the interleaved layout)
 //   2  general, G1 and G2 mixed otherwise (per query, scalar)
+//   9, 10  recipe alpha = 1 / alpha = 3 (one MUFU.RSQ per pair)
 template <int MODE, int QT>
 __device__ __forceinline__ f2 general_w(f2 d2, const QState<QT>& q, int r) {
+    if (MODE == 9) return rsq2(d2);           // recipe alpha = 1
+    if (MODE == 10) return cube2(rsq2(d2));   // recipe alpha = 3
     float lo, hi;
     up2(d2, lo, hi);
     if (MODE == 2) {
@@ -576,12 +635,12 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
             const f2 d1 = add2(fma2(bc2(Y.y), fy[r], fma2(bc2(X.y), fx[r], fq[r])), bc2(P.y));
             const f2 d2 = add2(fma2(bc2(Y.z), fy[r], fma2(bc2(X.z), fx[r], fq[r])), bc2(P.z));
             const f2 d3 = add2(fma2(bc2(Y.w), fy[r], fma2(bc2(X.w), fx[r], fq[r])), bc2(P.w));
-            if (MODE == 3 || MODE == 7 || MODE == 8) {
-                // a = d2^2 (alpha 4), d2 (alpha 2), a per-slot pick (mixed)
-                const f2 a0 = MODE == 3 ? mul2(d0, d0) : MODE == 7 ? d0 : recipe_a(d0, q.c[r]);
-                const f2 a1 = MODE == 3 ? mul2(d1, d1) : MODE == 7 ? d1 : recipe_a(d1, q.c[r]);
-                const f2 a2 = MODE == 3 ? mul2(d2, d2) : MODE == 7 ? d2 : recipe_a(d2, q.c[r]);
-                const f2 a3 = MODE == 3 ? mul2(d3, d3) : MODE == 7 ? d3 : recipe_a(d3, q.c[r]);
+            if (MODE == 3 || MODE == 7) {
+                // a = d2^2 (alpha 4), d2 (alpha 2)
+                const f2 a0 = MODE == 3 ? mul2(d0, d0) : d0;
+                const f2 a1 = MODE == 3 ? mul2(d1, d1) : d1;
+                const f2 a2 = MODE == 3 ? mul2(d2, d2) : d2;
+                const f2 a3 = MODE == 3 ? mul2(d3, d3) : d3;
                 const f2 r01 = rcp2(mul2(a0, a1));
                 sw[r] = fma2(r01, add2(a0, a1), sw[r]);
                 swz[r] = fma2(r01, fma2(a1, bc2(Z.x), mul2(a0, bc2(Z.y))), swz[r]);
@@ -594,6 +653,35 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
                     sw[r] = add2(sw[r], w2);
                     swz[r] = fma2(w2, bc2(Z.z), swz[r]);
                     const f2 w3 = rcp2(a3);
+                    sw[r] = add2(sw[r], w3);
+                    swz[r] = fma2(w3, bc2(Z.w), swz[r]);
+                }
+            } else if (MODE == 8) {
+                // mixed recipe warp: both the paired (alpha 4 / 2) and the
+                // rsqrt (alpha 1 / 3) forms, picked per slot
+                const f2 code = q.c[r];
+                const f2 a0 = recipe_a(d0, code), a1 = recipe_a(d1, code);
+                const f2 a2 = recipe_a(d2, code), a3 = recipe_a(d3, code);
+                const f2 v0 = recipe_rsq(d0, code), v1 = recipe_rsq(d1, code);
+                const f2 v2 = recipe_rsq(d2, code), v3 = recipe_rsq(d3, code);
+                const f2 r01 = rcp2(mul2(a0, a1));
+                sw[r] = sel_paired(code, fma2(r01, add2(a0, a1), sw[r]),
+                                   add2(add2(sw[r], v0), v1));
+                swz[r] = sel_paired(code,
+                                    fma2(r01, fma2(a1, bc2(Z.x), mul2(a0, bc2(Z.y))), swz[r]),
+                                    fma2(v1, bc2(Z.y), fma2(v0, bc2(Z.x), swz[r])));
+                if (pair23) {
+                    const f2 r23 = rcp2(mul2(a2, a3));
+                    sw[r] = sel_paired(code, fma2(r23, add2(a2, a3), sw[r]),
+                                       add2(add2(sw[r], v2), v3));
+                    swz[r] = sel_paired(code,
+                                        fma2(r23, fma2(a3, bc2(Z.z), mul2(a2, bc2(Z.w))), swz[r]),
+                                        fma2(v3, bc2(Z.w), fma2(v2, bc2(Z.z), swz[r])));
+                } else {
+                    const f2 w2 = sel_paired(code, rcp2(a2), v2);
+                    sw[r] = add2(sw[r], w2);
+                    swz[r] = fma2(w2, bc2(Z.z), swz[r]);
+                    const f2 w3 = sel_paired(code, rcp2(a3), v3);
                     sw[r] = add2(sw[r], w3);
                     swz[r] = fma2(w3, bc2(Z.w), swz[r]);
                 }
@@ -638,9 +726,9 @@ __device__ __forceinline__ void k4_near_point(float pxh, float pyh, float pxl, f
             w = rcp2(mul2(d2, d2));
         } else if (MODE == 7) {  // alpha == 2: s == 1
             w = rcp2(d2);
-        } else if (MODE == 8) {  // mixed recipe: t = d2 s, a = t^2 or t per slot
+        } else if (MODE == 8) {  // mixed recipe: t = d2 s (s == 1 unless alpha 4), per slot
             d2 = mul2(d2, q.s[r]);
-            w = rcp2(recipe_a(d2, q.c[r]));
+            w = sel_paired(q.c[r], rcp2(recipe_a(d2, q.c[r])), recipe_rsq(d2, q.c[r]));
         } else {
             w = general_w<MODE, QT>(d2, q, r);
         }
@@ -770,7 +858,8 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t wbase = q0 + cta * (kK4Threads * kQT) + static_cast<size_t>(warp) * (32 * kQT);
     QState<kQT> q;
-    bool any_g1 = false, any_g2 = false, any_scaled = false, any_r2 = false, any_r4 = false;
+    bool any_g1 = false, any_g2 = false, any_scaled = false;
+    unsigned rcodes = 0;  // recipe class codes present (bit per code)
     {
         float4 r[kQT];
 #pragma unroll
@@ -780,8 +869,7 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
             q.v[i] = p < q1;
             if (q.v[i]) r[i] = a.qpar[p];
             q.g2[i] = r[i].w == 2.0f;
-            any_r2 |= q.v[i] && r[i].w == 3.0f;
-            any_r4 |= q.v[i] && r[i].w == 1.0f;
+            if (RECIPE && q.v[i]) rcodes |= 1u << static_cast<int>(r[i].w);
             any_g2 |= q.v[i] && q.g2[i];
             any_g1 |= q.v[i] && !q.g2[i];
             any_scaled |= q.v[i] && r[i].z != 1.0f;
@@ -797,11 +885,15 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
     any_g1 = __any_sync(0xFFFFFFFFu, any_g1);
     any_g2 = __any_sync(0xFFFFFFFFu, any_g2);
     any_scaled = __any_sync(0xFFFFFFFFu, any_scaled);
-    any_r2 = __any_sync(0xFFFFFFFFu, any_r2);
-    any_r4 = __any_sync(0xFFFFFFFFu, any_r4);
+    rcodes = __reduce_or_sync(0xFFFFFFFFu, rcodes);
     int mode;
     if (RECIPE) {
-        mode = any_r2 ? (any_r4 ? 8 : 7) : (any_scaled ? 0 : 3);
+        // one class in the warp: its pure mode; several: the per-slot form
+        mode = rcodes == (1u << 3)  ? 7
+             : rcodes == (1u << 4)  ? 9
+             : rcodes == (1u << 5)  ? 10
+             : rcodes == (1u << 1) || rcodes == 0 ? (any_scaled ? 0 : 3)
+                                    : 8;
 #ifdef AIDW_K4_FORCE_MIXED
         mode = 8;
 #endif
@@ -853,6 +945,8 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
             if (mode == 3) k4_tile<3, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
             else if (mode == 7) k4_tile<7, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
             else if (mode == 8) k4_tile<8, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
+            else if (mode == 9) k4_tile<9, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
+            else if (mode == 10) k4_tile<10, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
             else k4_tile<0, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
         } else {
             if (mode == 5) k4_tile<5, kQT>(tt, q, a.qhl, wbase, lane, q1, nq, any_far, any_near, tg.x, tg.y, SW, SWZ);
@@ -1016,7 +1110,12 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     border.release();
 
     DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), flag_g2(q.n, s), scan_g2(q.n, s), order_q(q.n, s),
-        flag_a2(q.n, s), scan_a2(q.n, s);
+        sub_flags(kRecipeSubs * q.n, s), sub_scans(kRecipeSubs * q.n, s);
+    RecipeFlags rf;
+    for (int k = 0; k < kRecipeSubs; ++k) {
+        rf.flag[k] = sub_flags.get() + k * q.n;
+        rf.scan[k] = sub_scans.get() + k * q.n;
+    }
     DBuf<float4> qhl(q.n, s), qpar(q.n, s);
     DBuf<double> lshift(q.n, s);
     DBuf<uint32_t> zkey(q.n, s), zpos(q.n, s);
@@ -1032,13 +1131,13 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
         return static_cast<unsigned>(std::fmin(share, 1.0) * 4294967295.0);
     }();
     LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f,
-           g_alpha4_recipe.load() ? 1 : 0, g2_threshold, zpos.get(), flag.get(), flag_a2.get(),
+           g_alpha4_recipe.load() ? 1 : 0, g2_threshold, zpos.get(), flag.get(), rf,
            flag_g2.get());
     exclusive_scan_u32(flag.get(), scan_a.get(), q.n, s);
-    exclusive_scan_u32(flag_a2.get(), scan_a2.get(), q.n, s);
+    for (int k = 0; k < kRecipeSubs; ++k) exclusive_scan_u32(rf.flag[k], rf.scan[k], q.n, s);
     exclusive_scan_u32(flag_g2.get(), scan_g2.get(), q.n, s);
     LAUNCH(query_records_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, zpos.get(),
-           flag.get(), scan_a.get(), flag_a2.get(), scan_a2.get(), flag_g2.get(), scan_g2.get(), order_q.get(), qhl.get(), qpar.get(),
+           flag.get(), scan_a.get(), rf, flag_g2.get(), scan_g2.get(), order_q.get(), qhl.get(), qpar.get(),
            lshift.get(), times ? times->d_alpha4 : nullptr);
 
     DBuf<double2> part(q.n * sp.chunks, s);

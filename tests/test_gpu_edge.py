@@ -86,7 +86,7 @@ def test_param_variants_vs_oracle(params):
     assert np.max(np.abs(out64.result.predicted - ref["pred"]) / np.abs(ref["pred"])) <= 2e-11
 
 
-@pytest.mark.parametrize("alpha", [0.5, 1.0, 1.7, 2.0, 4.0, 8.0])
+@pytest.mark.parametrize("alpha", [0.5, 1.0, 1.7, 2.0, 3.0, 4.0, 8.0])
 def test_idw_mode_vs_oracle(alpha):
     data = A.generate_random_points(20_000, UNIT, 3, "planar")
     q = A.generate_random_queries(700, UNIT, 4)
@@ -97,18 +97,23 @@ def test_idw_mode_vs_oracle(alpha):
 
 
 @pytest.mark.parametrize("scale", [1.0, 1e-3])
-def test_mixed_recipe_classes_alpha2_alpha4(scale):
-    # levels saturating at exactly 2 and 4 on clustered data: warps mix the
-    # w = 1/d^2 and w = 1/d^4 recipe classes with general-alpha queries; a
-    # small domain exercises the per-query ratio scaling (s != 1) of alpha 4
+@pytest.mark.parametrize("levels,exact", [((2.0, 2.0, 3.0, 4.0, 4.0), (2.0, 4.0)),
+                                          ((1.0, 1.0, 3.0, 3.0, 4.0), (1.0, 3.0, 4.0)),
+                                          ((1.0, 1.0, 2.0, 2.0, 3.0), (1.0, 2.0, 3.0))])
+def test_mixed_recipe_classes(scale, levels, exact):
+    # levels saturating at exact integers on clustered data: warps mix the
+    # recipe classes (alpha = 1, 2, 3, 4) with each other and with
+    # general-alpha queries; a small domain exercises the per-query ratio
+    # scaling (s != 1) of alpha 4
     xs, ys, zs = O.generate_clustered(30_000, seed=11)
     xs, ys = xs * scale, ys * scale
     qx, qy = O.generate_queries(3000, (0.0, 0.0, scale, scale), 12)
-    p = A.AidwParams(k=10, alpha_levels=(2.0, 2.0, 3.0, 4.0, 4.0))
+    p = A.AidwParams(k=10, alpha_levels=levels)
     out = A.run_pipeline(A.PointSet(xs, ys, zs), A.PointSet(qx, qy), A.RunConfig(params=p))
     ref = O.pipeline(xs, ys, zs, qx, qy, k=10, variant=1, levels=p.alpha_levels)
     assert np.max(np.abs(out.result.alphas - ref["alpha"]) / ref["alpha"]) <= 1e-12
-    assert np.any(out.result.alphas == 2.0) and np.any(out.result.alphas == 4.0)
+    for a in exact:
+        assert np.any(out.result.alphas == a)
     assert pred_err(out.result.predicted, ref["pred"], zs) <= 1e-5
 
 

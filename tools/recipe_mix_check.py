@@ -1,5 +1,5 @@
 """Recipe-class mixing check (GPU box): AIDW with alpha levels saturating at
-exactly 2 and 4 on clustered data, so warps of the alpha = 4 / alpha = 2
+exactly 1, 2, 3 and 4 on clustered data, so warps of the alpha = 4 / 2 / 1 / 3
 recipe regions and the general region meet; prints the worst contract errors
 against the C oracle.  Run it against a library built with
 -DAIDW_K4_FORCE_MIXED=1 (tools/build_variant.sh, AIDW_LIB_PATH) to force
@@ -11,7 +11,8 @@ def pe(got, ref, zs):
     return np.abs(got - ref) / np.maximum(np.abs(ref), 1e-3 * span)
 xs, ys, zs = O.generate_clustered(30_000, seed=11)
 qx, qy = O.generate_queries(3000, (0.0, 0.0, 1.0, 1.0), 12)
-for lv in [(2.0, 2.0, 3.0, 4.0, 4.0), (4.0,4.0,4.0,4.0,4.0), (2.0,)*5]:
+for lv in [(2.0, 2.0, 3.0, 4.0, 4.0), (1.0, 1.0, 3.0, 3.0, 4.0), (1.0, 1.0, 2.0, 2.0, 3.0),
+           (4.0,) * 5, (2.0,) * 5, (1.0,) * 5, (3.0,) * 5]:
     p = A.AidwParams(k=10, alpha_levels=lv)
     ref = O.pipeline(xs, ys, zs, qx, qy, k=10, variant=1, levels=lv)
     out = A.run_pipeline(A.PointSet(xs, ys, zs), A.PointSet(qx, qy), A.RunConfig(params=p))
