@@ -37,6 +37,7 @@
 namespace aidwb {
 
 std::atomic<long long> g_launches{0};
+thread_local Arena* t_arena = nullptr;
 
 namespace {
 
@@ -594,10 +595,61 @@ void lattice_device(size_t nx, size_t ny, const double* bbox, size_t row0, size_
                bbox[1], sx, sy, row0, rows, d_qx, d_qy);
 }
 
+// Per-call workspace (see DBuf): a cached device buffer per device, sized
+// by the largest call so far (plus what overflowed), handed to one call at
+// a time.  Recycled after the call's stream is synchronised.
+struct ArenaCache {
+    std::mutex mu;
+    std::vector<Arena> free_list;
+};
+ArenaCache g_arena_cache[64];
+
+struct ArenaScope {
+    Arena a;
+    Arena* prev = nullptr;
+    int dev = 0;
+    explicit ArenaScope(cudaStream_t s) {
+        CK(cudaGetDevice(&dev));
+        {
+            std::lock_guard<std::mutex> lock(g_arena_cache[dev & 63].mu);
+            auto& fl = g_arena_cache[dev & 63].free_list;
+            if (!fl.empty()) {
+                a = fl.back();
+                fl.pop_back();
+            }
+        }
+        a.used = a.overflow = 0;
+        a.stream = s;
+        prev = t_arena;
+        t_arena = &a;
+    }
+    ~ArenaScope() {
+        t_arena = prev;
+        // normally a no-op (the call synchronised); on an exception path it
+        // keeps in-flight kernels off a recycled workspace
+        if (cudaStreamSynchronize(a.stream) != cudaSuccess) cudaGetLastError();
+        if (a.overflow) {  // grow for the next call (the pool keeps the memory warm)
+            if (a.base) cudaFree(a.base);
+            a.base = nullptr;
+            a.cap = 0;
+            const size_t want = ((a.used + a.overflow) * 5 / 4 + (size_t(1) << 20)) & ~size_t(255);
+            if (cudaMalloc(reinterpret_cast<void**>(&a.base), want) == cudaSuccess) a.cap = want;
+            else cudaGetLastError();
+        }
+        a.used = a.overflow = 0;
+        a.stream = nullptr;
+        std::lock_guard<std::mutex> lock(g_arena_cache[dev & 63].mu);
+        g_arena_cache[dev & 63].free_list.push_back(a);
+    }
+    ArenaScope(const ArenaScope&) = delete;
+    ArenaScope& operator=(const ArenaScope&) = delete;
+};
+
 void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_stats* st,
                     cudaStream_t s, double h2d_ms, const std::chrono::steady_clock::time_point& t0,
                     double* h_pred, double* h_alpha) {
     const long long launches0 = g_launches.load();
+    ArenaScope arena(s);  // declared first: destroyed after every DBuf of the call
     Events ev;
     std::vector<cudaEvent_t> marks;
     cudaEvent_t k4b = nullptr, k4e = nullptr, knnb = nullptr, knne = nullptr;

@@ -42,25 +42,51 @@ extern std::atomic<long long> g_launches;
     } while (0)
 
 // ------------------------------------------------------------------ workspace
-// Stream-ordered device buffers from the default memory pool (kept warm by
-// a release threshold set once per device, see capi.cu).
+// Stream-ordered device buffers.  Inside a pipeline call (ArenaScope in
+// capi.cu) they are bump-allocated from one cached per-call workspace on the
+// call's stream — no allocator API call per buffer, no reuse within the call
+// (so no aliasing); the workspace is recycled only after the call's stream
+// has synchronised.  Elsewhere, or when the workspace is full, they come
+// from the default memory pool (kept warm by a release threshold set once per
+// device, see capi.cu).
+struct Arena {
+    char* base = nullptr;
+    size_t cap = 0, used = 0, overflow = 0;
+    cudaStream_t stream = nullptr;
+};
+extern thread_local Arena* t_arena;
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
     cudaStream_t s = nullptr;
+    bool pooled = true;  // false: carved from the call's arena
     DBuf() = default;
     DBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
     void alloc(size_t count, cudaStream_t stream) {
         release();
         s = stream;
         n = count;
-        if (count) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+        if (!count) return;
+        const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+        Arena* a = t_arena;
+        if (a && a->stream == stream) {
+            if (a->used + bytes <= a->cap) {
+                p = reinterpret_cast<T*>(a->base + a->used);
+                a->used += bytes;
+                pooled = false;
+                return;
+            }
+            a->overflow += bytes;  // grow the workspace for the next call
+        }
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
     }
     void release() {
-        if (p) cudaFreeAsync(p, s);
+        if (p && pooled) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
+        pooled = true;
     }
     ~DBuf() { release(); }
     DBuf(const DBuf&) = delete;
