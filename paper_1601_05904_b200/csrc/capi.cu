@@ -628,13 +628,16 @@ struct ArenaScope {
         // normally a no-op (the call synchronised); on an exception path it
         // keeps in-flight kernels off a recycled workspace
         if (cudaStreamSynchronize(a.stream) != cudaSuccess) cudaGetLastError();
-        if (a.overflow) {  // grow for the next call (the pool keeps the memory warm)
-            if (a.base) cudaFree(a.base);
+        if (a.overflow) {  // grow for the next call, from the warm pool
+            if (a.base) cudaFreeAsync(a.base, a.stream);
             a.base = nullptr;
             a.cap = 0;
             const size_t want = ((a.used + a.overflow) * 5 / 4 + (size_t(1) << 20)) & ~size_t(255);
-            if (cudaMalloc(reinterpret_cast<void**>(&a.base), want) == cudaSuccess) a.cap = want;
-            else cudaGetLastError();
+            if (cudaMallocAsync(reinterpret_cast<void**>(&a.base), want, a.stream) == cudaSuccess &&
+                cudaStreamSynchronize(a.stream) == cudaSuccess)
+                a.cap = want;
+            else
+                cudaGetLastError();
         }
         a.used = a.overflow = 0;
         a.stream = nullptr;
