@@ -60,9 +60,6 @@ constexpr int kK4Threads = AIDW_K4_THREADS;
 #ifndef AIDW_K4_MIXPAIRS
 #define AIDW_K4_MIXPAIRS 0
 #endif
-#ifndef AIDW_K4_NEAR_KAHAN_SW
-#define AIDW_K4_NEAR_KAHAN_SW 1
-#endif
 #ifndef AIDW_K4_FAR_UNROLL
 #define AIDW_K4_FAR_UNROLL 2
 #endif
@@ -732,16 +729,12 @@ __device__ __forceinline__ void k4_near_point(float pxh, float pyh, float pxl, f
         } else {
             w = general_w<MODE, QT>(d2, q, r);
         }
-#if AIDW_K4_NEAR_KAHAN_SW
         {
             const f2 yw = sub2(w, cw[r]);
             const f2 s1 = add2(sw[r], yw);
             cw[r] = sub2(sub2(s1, sw[r]), yw);
             sw[r] = s1;
         }
-#else
-        sw[r] = add2(sw[r], w);
-#endif
         const f2 tz = fma2(w, bc2(pzh), mul2(w, bc2(pzl)));
         const f2 y = sub2(tz, cz[r]);
         const f2 s2 = add2(swz[r], y);
@@ -826,10 +819,8 @@ __device__ __forceinline__ void k4_tile(const float* __restrict__ t, const QStat
             up2(sw[r], w0, w1);
             up2(swz[r], z0, z1);
             up2(cz[r], c0, c1);
-            float e0 = 0.0f, e1 = 0.0f;
-#if AIDW_K4_NEAR_KAHAN_SW
+            float e0, e1;
             up2(cw[r], e0, e1);
-#endif
             if (nq[2 * r])
                 SW[2 * r] += static_cast<double>(w0) - static_cast<double>(e0),
                     SWZ[2 * r] += static_cast<double>(z0) - static_cast<double>(c0);
