@@ -342,10 +342,10 @@ def main():
     # XU pipe 16 MUFU ops; a class is bound by the slower of the two.
     #   recipe (alpha == 4): 3 (d2) + 1 (d2^2) + 2.5 (pair/single sums) = 6.5
     #     FP32 + 0.75 MUFU per pair (two of every four points share one rcp)
-    #   general: G1 6 FP32 + 2 MUFU (lg2, ex2), G2 15 FP32 + 1 MUFU (ex2 as a
-    #     degree-6 polynomial); G1 / G2 split ~1:1 by coordinate hash
+    #   general: G1 6 FP32 + 2 MUFU (lg2, ex2), G2 14 FP32 + 1 MUFU (ex2 as a
+    #     degree-5 polynomial); G1 / G2 split ~1:1 by coordinate hash
     clk_recipe = max(6.5 / 128, 0.75 / 16)
-    clk_general = max(0.5 * (6 + 15) / 128, 0.5 * (2 + 1) / 16)
+    clk_general = max(0.5 * (6 + 14) / 128, 0.5 * (2 + 1) / 16)
     clk_mix = (a4 * clk_recipe + (n - a4) * clk_general) / n
     peak_mix = sms * f_mhz * 1e6 / clk_mix / 1e9
     peak_general = sms * f_mhz * 1e6 / clk_general / 1e9
@@ -414,15 +414,15 @@ def main():
                          "peak_def": f"{sms} SMs x {f_mhz:.0f} MHz ({pk['source']} sm_max_mhz) / "
                                      f"{clk_mix:.4f} SM-clk per pair: executed mix of the "
                                      f"alpha=4 recipe ({a4} queries; FMA-bound 6.5 FP32 + "
-                                     f"0.75 MUFU) and general alpha (MUFU-bound 10.5 FP32 + "
+                                     f"0.75 MUFU) and general alpha (MUFU-bound 10 FP32 + "
                                      f"1.5 MUFU) far-tile forms; 128 FP32 + 16 MUFU per SM-clk",
                          "frac_vs_2mufu_roofline": achieved / peak_gpairs,
                          "fp32_view": {  # the same bound as FP32 op throughput
                              "unit": "TFLOP/s (FP32 ops, FFMA = 1)",
-                             "ops_per_pair": (a4 * 6.5 + (n - a4) * 10.5) / n,
-                             "achieved": achieved * 1e9 * (a4 * 6.5 + (n - a4) * 10.5) / n / 1e12,
+                             "ops_per_pair": (a4 * 6.5 + (n - a4) * 10.0) / n,
+                             "achieved": achieved * 1e9 * (a4 * 6.5 + (n - a4) * 10.0) / n / 1e12,
                              "peak": sms * 128 * f_mhz * 1e6 / 1e12,
-                             "frac": achieved * 1e9 * (a4 * 6.5 + (n - a4) * 10.5) / n /
+                             "frac": achieved * 1e9 * (a4 * 6.5 + (n - a4) * 10.0) / n /
                                      (sms * 128 * f_mhz * 1e6)},
                          "alpha4_recipe_queries": a4, "pairs_per_launch": pairs,
                          "k4_ms": k4_ms},
