@@ -195,6 +195,33 @@ def test_deterministic_and_shard_invariant():
     assert np.array_equal(again.predicted, full.predicted)
 
 
+def test_workspace_reuse_across_sizes_and_threads():
+    """The per-call device workspace (bump-allocated temporaries, recycled
+    after each call, grown after an overflowing call): small -> large ->
+    small calls, and calls from concurrent host threads, reproduce the bits
+    of the first evaluation."""
+    import threading
+    small_d, small_q = A.generate_random_points(20_000, UNIT, 21), A.generate_random_queries(3000, UNIT, 22)
+    big_d, big_q = A.generate_random_points(300_000, UNIT, 23), A.generate_random_queries(40_000, UNIT, 24)
+    cfg = A.RunConfig(params=A.AidwParams(k=10))
+    ref_small = A.run_pipeline(small_d, small_q, cfg).result.predicted
+    ref_big = A.run_pipeline(big_d, big_q, cfg).result.predicted  # overflows, grows
+    assert np.array_equal(A.run_pipeline(small_d, small_q, cfg).result.predicted, ref_small)
+    assert np.array_equal(A.run_pipeline(big_d, big_q, cfg).result.predicted, ref_big)
+    out = {}
+
+    def work(i):
+        d, q, ref = (small_d, small_q, ref_small) if i % 2 else (big_d, big_q, ref_big)
+        out[i] = np.array_equal(A.run_pipeline(d, q, cfg).result.predicted, ref)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert all(out.values()) and len(out) == 4
+
+
 @pytest.mark.parametrize("m", [2, 255, 256, 257, 2047, 2048, 2049, 4097, 262_144, 262_145])
 def test_tile_and_chunk_boundaries(m):
     """Data sizes at the K4 tile (256), chunk-split (8 tiles per chunk, 64
