@@ -186,7 +186,8 @@ void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, cons
                           cudaStream_t s);
 
 // Generic exclusive scan of n uint32 values (in place allowed).
-void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, size_t n, cudaStream_t s);
+void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, size_t n, cudaStream_t s,
+                        uint32_t* d_copy = nullptr);
 
 // Stable LSD radix sort of (key, value) u32 pairs on the low `bits` bits.
 void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaStream_t s);

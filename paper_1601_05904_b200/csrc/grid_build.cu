@@ -92,7 +92,7 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 
 __global__ void __launch_bounds__(kThreads) scan_onepass_kernel(
     const uint32_t* in, uint32_t* out, size_t n, unsigned long long* __restrict__ status,
-    unsigned* __restrict__ ticket) {
+    unsigned* __restrict__ ticket, uint32_t* __restrict__ copy) {
     __shared__ unsigned s_tile;
     __shared__ uint32_t s_warp[kThreads / 32];
     __shared__ uint32_t s_prefix;
@@ -152,7 +152,10 @@ __global__ void __launch_bounds__(kThreads) scan_onepass_kernel(
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
         const size_t idx = base + static_cast<size_t>(j) * 32 + lane;
-        if (idx < n) out[idx] = v[j] + add;
+        if (idx < n) {
+            out[idx] = v[j] + add;
+            if (copy) copy[idx] = v[j] + add;
+        }
     }
 }
 
@@ -392,15 +395,15 @@ __global__ void cell_rank_small_kernel(const uint32_t* __restrict__ cell_start,
 // One warp per queued cell of kSmallCell < n <= kMidCell points: the ids go
 // to a per-warp shared buffer and each lane places its ids by rank (the
 // number of smaller ids in the cell; ids are distinct), then the gather.
-__global__ void __launch_bounds__(256) cell_sort_mid_kernel(
+__device__ __forceinline__ void sort_mid_cells(
+    unsigned block, unsigned nblocks, uint32_t (*buf)[kMidCell],
     const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ mid,
     const uint32_t* __restrict__ nmid, const uint32_t* __restrict__ scattered,
     const double* __restrict__ x, const double* __restrict__ y, uint32_t* __restrict__ ids,
     double2* __restrict__ sxy, double* __restrict__ sx, double* __restrict__ sy) {
-    __shared__ uint32_t buf[8][kMidCell];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + wp; w < *nmid; w += warps) {
+    const uint32_t warps = nblocks * (blockDim.x >> 5);
+    for (uint32_t w = block * (blockDim.x >> 5) + wp; w < *nmid; w += warps) {
         const uint32_t c = mid[w];
         const uint32_t b = cell_start[c], n = cell_start[c + 1] - b;
         for (uint32_t j = lane; j < n; j += 32) buf[wp][j] = scattered[b + j];
@@ -420,15 +423,14 @@ __global__ void __launch_bounds__(256) cell_sort_mid_kernel(
 // gather.  A cell above kBigCell (degenerate, heavily duplicated data) is
 // instead rebuilt by a stable compaction of the key array in index order —
 // O(m) for that cell, correct for any size, no host round trip.
-__global__ void __launch_bounds__(256) cell_sort_big_kernel(
+__device__ __forceinline__ void sort_big_cells(
+    unsigned block, unsigned nblocks, uint32_t* v, uint32_t* wsum,
     const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ big,
     const uint32_t* __restrict__ nbig, const uint32_t* __restrict__ scattered,
     const uint32_t* __restrict__ keys, size_t m, const double* __restrict__ x,
     const double* __restrict__ y, uint32_t* __restrict__ ids, double2* __restrict__ sxy,
     double* __restrict__ sx, double* __restrict__ sy) {
-    __shared__ uint32_t v[kBigCell];
-    __shared__ uint32_t wsum[8];
-    for (uint32_t w = blockIdx.x; w < *nbig; w += gridDim.x) {
+    for (uint32_t w = block; w < *nbig; w += nblocks) {
         const uint32_t c = big[w];
         const uint32_t b = cell_start[c], n = cell_start[c + 1] - b;
         __syncthreads();
@@ -481,6 +483,26 @@ __global__ void __launch_bounds__(256) cell_sort_big_kernel(
     }
 }
 
+// One launch for both crowded-cell queues: CTAs [0, kMidCtas) take the
+// warp-sized cells, the rest the CTA-sized ones (role uniform per CTA).
+constexpr unsigned kMidCtas = 148u * 4u, kBigCtas = 148u * 2u;
+__global__ void __launch_bounds__(256) cell_sort_crowded_kernel(
+    const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ mid,
+    const uint32_t* __restrict__ big, const uint32_t* __restrict__ nbig,
+    const uint32_t* __restrict__ scattered, const uint32_t* __restrict__ keys, size_t m,
+    const double* __restrict__ x, const double* __restrict__ y, uint32_t* __restrict__ ids,
+    double2* __restrict__ sxy, double* __restrict__ sx, double* __restrict__ sy) {
+    __shared__ uint32_t buf[8][kMidCell];
+    __shared__ uint32_t v[kBigCell];
+    __shared__ uint32_t wsum[8];
+    if (blockIdx.x < kMidCtas)
+        sort_mid_cells(blockIdx.x, kMidCtas, buf, cell_start, mid, nbig, scattered, x, y, ids,
+                       sxy, sx, sy);
+    else
+        sort_big_cells(blockIdx.x - kMidCtas, gridDim.x - kMidCtas, v, wsum, cell_start, big,
+                       nbig + 1, scattered, keys, m, x, y, ids, sxy, sx, sy);
+}
+
 // Blocked cell order (K4 data tiles): cells visited in 8 x 8-cell blocks,
 // blocks row-major, cells row-major inside a block.  On a factor-4 grid a
 // block holds ~256 points (16 r_exp^2 m / A = 4 points per cell), so a
@@ -526,14 +548,15 @@ int bits_for(uint64_t max_key) {
 
 }  // namespace
 
-void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, size_t n, cudaStream_t s) {
+void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, size_t n, cudaStream_t s,
+                        uint32_t* d_copy) {
     if (n == 0) return;
     const unsigned tiles = ceil_div(n, kScanTile);
     // status words (one per tile) + the tile ticket, zeroed together
     DBuf<unsigned long long> status(static_cast<size_t>(tiles) + 1, s);
     CK(cudaMemsetAsync(status.get(), 0, (static_cast<size_t>(tiles) + 1) * sizeof(unsigned long long), s));
     LAUNCH(scan_onepass_kernel, tiles, kThreads, 0, s, d_in, d_out, n, status.get(),
-           reinterpret_cast<unsigned*>(status.get() + tiles));
+           reinterpret_cast<unsigned*>(status.get() + tiles), d_copy);
 }
 
 void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaStream_t s) {
@@ -591,28 +614,24 @@ void build_grid_device(const double* d_x, const double* d_y, size_t m,
         out.sorted_x.alloc(m, s);
         out.sorted_y.alloc(m, s);
     }
-    DBuf<uint32_t> keys(m, s), vals(m, s), cursor(cells, s), mid(cells, s), big(cells, s),
+    DBuf<uint32_t> keys(m, s), vals(m, s), cursor(cells + 1, s), mid(cells, s), big(cells, s),
         nbig(2, s);
     CK(cudaMemsetAsync(out.cell_start.get(), 0, (cells + 1) * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(nbig.get(), 0, 2 * sizeof(uint32_t), s));
     LAUNCH(cell_ids_kernel, ceil_div(m, kThreads), kThreads, 0, s, d_x, d_y, m, g, keys.get(),
            static_cast<uint32_t*>(nullptr), out.cell_start.get(), d_fail);
-    exclusive_scan_u32(out.cell_start.get(), out.cell_start.get(), cells + 1, s);
-    // counting sort: cursors start at cell_start; vals receives the scatter
-    CK(cudaMemcpyAsync(cursor.get(), out.cell_start.get(), cells * sizeof(uint32_t),
-                       cudaMemcpyDeviceToDevice, s));
+    // counting sort: cursors start at cell_start (written by the same scan,
+    // cells + 1 entries); vals receives the scatter
+    exclusive_scan_u32(out.cell_start.get(), out.cell_start.get(), cells + 1, s, cursor.get());
     LAUNCH(cell_scatter_kernel, ceil_div(m, kThreads), kThreads, 0, s, keys.get(), m,
            cursor.get(), vals.get());
     LAUNCH(cell_rank_small_kernel, ceil_div(m, kThreads), kThreads, 0, s,
            out.cell_start.get(), keys.get(), m, vals.get(), d_x, d_y, out.sorted_ids.get(),
            out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get(), mid.get(), big.get(),
            nbig.get());
-    LAUNCH(cell_sort_mid_kernel, 148u * 4u, 256, 0, s, out.cell_start.get(), mid.get(),
-           nbig.get(), vals.get(), d_x, d_y, out.sorted_ids.get(), out.sorted_xy.get(),
-           out.sorted_x.get(), out.sorted_y.get());
-    LAUNCH(cell_sort_big_kernel, 148u * 2u, 256, 0, s, out.cell_start.get(), big.get(),
-           nbig.get() + 1, vals.get(), keys.get(), m, d_x, d_y, out.sorted_ids.get(),
-           out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get());
+    LAUNCH(cell_sort_crowded_kernel, kMidCtas + kBigCtas, 256, 0, s, out.cell_start.get(),
+           mid.get(), big.get(), nbig.get(), vals.get(), keys.get(), m, d_x, d_y,
+           out.sorted_ids.get(), out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get());
 }
 
 void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, const GridGeom& g,
