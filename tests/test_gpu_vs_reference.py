@@ -75,3 +75,16 @@ def test_idw_pipeline_matches_reference(alpha):
                          A.RunConfig(mode="idw", alpha=alpha))
     assert np.all(out.result.alphas == alpha)
     assert contract(out.result.predicted, ref_pred, zs) <= 1e-5
+
+
+@pytest.mark.parametrize("kind", ["uniform", "clustered"])
+def test_bench_scale_data_matches_reference(kind):
+    """BASELINE configs[2] / [3] data size (1M points: 3907 K4 tiles in 32
+    data chunks, the bench's grid) against the reference on 4096 queries."""
+    need_ref()
+    xs, ys, zs, qx, qy = inputs(kind, 1_000_000, 4096, 42)
+    ref_pred, ref_alpha, _, _ = O.ref_run_pipeline(xs, ys, zs, qx, qy, mode=1, k=10)
+    out = A.run_pipeline(A.PointSet(xs, ys, zs), A.PointSet(qx, qy),
+                         A.RunConfig(params=A.AidwParams(k=10)))
+    assert np.max(np.abs(out.result.alphas - ref_alpha) / ref_alpha) <= 1e-12
+    assert contract(out.result.predicted, ref_pred, zs) <= 1e-5
