@@ -444,7 +444,8 @@ __global__ void __launch_bounds__(128) knn_brute_kernel(KnnArgs a) {
         }                                                           \
         AIDW_KNN_CASE(KERNEL, 2) AIDW_KNN_CASE(KERNEL, 4)           \
         AIDW_KNN_CASE(KERNEL, 8) AIDW_KNN_CASE(KERNEL, 10)          \
-        AIDW_KNN_CASE(KERNEL, 12) AIDW_KNN_CASE(KERNEL, 16)         \
+        AIDW_KNN_CASE(KERNEL, 12) AIDW_KNN_CASE(KERNEL, 15)         \
+        AIDW_KNN_CASE(KERNEL, 16)                                   \
         AIDW_KNN_CASE(KERNEL, 24) AIDW_KNN_CASE(KERNEL, 32)         \
         AIDW_KNN_CASE(KERNEL, 48) AIDW_KNN_CASE(KERNEL, 64)         \
         else {                                                      \
