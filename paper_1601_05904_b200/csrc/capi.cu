@@ -231,15 +231,18 @@ Extents extents(const double* ax, const double* ay, size_t na, const double* bx,
     return Extents{Box{h[0], h[1], h[2], h[3]}, h[4], h[5]};
 }
 
+__global__ void fail_init_kernel(long long* __restrict__ d) {
+    if (threadIdx.x < 4) d[threadIdx.x] = LLONG_MAX;
+}
+
 // Failure indices written by kernels (atomicMin), resolved after sync.
+// Initialised on the stream by a one-warp kernel (no host round trip).
 struct FailFlags {
     DBuf<long long> d;
     long long h[4];
     explicit FailFlags(cudaStream_t s) : d(4, s) {
-        const long long init[4] = {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MAX};
-        std::memcpy(h, init, sizeof h);
-        CK(cudaMemcpyAsync(d.get(), h, sizeof h, cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));  // h is reused as the D2H target
+        for (long long& v : h) v = LLONG_MAX;
+        LAUNCH(fail_init_kernel, 1, 32, 0, s, d.get());
     }
     long long* slot(int i) { return d.get() + i; }
     void fetch(cudaStream_t s) {
