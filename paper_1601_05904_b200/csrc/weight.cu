@@ -1046,7 +1046,8 @@ void set_alpha4_recipe(bool enabled) { g_alpha4_recipe.store(enabled); }
 WeightSplit weight_split(size_t m) {
     // Data chunks per query (the grid's y dimension): enough CTAs to fill
     // 148 SMs at small n without a partial last wave dominating — up to 64
-    // chunks of >= 4 tiles while m <= 256K, 32 chunks beyond (partials
+    // chunks (one tile each for m <= 16K: 10K x 10K 0.23 -> 0.10 ms) while
+    // m <= 256K, 32 chunks beyond (partials
     // 512 B per query; 32 vs 16: -0.6 % K4 time at 1M x 1M).  A function of m only, so a query's summation order
     // never depends on n, the shard or the GPU count.
     WeightSplit w;
@@ -1055,7 +1056,7 @@ WeightSplit weight_split(size_t m) {
     const size_t cap = w.tiles <= 1024 ? 64 : static_cast<size_t>(kMaxChunks);
     static const size_t min_tiles = [] {  // AIDW_K4_CHUNK_TILES: tuning only
         const char* v = std::getenv("AIDW_K4_CHUNK_TILES");
-        return static_cast<size_t>(v ? std::max(1, std::atoi(v)) : 4);
+        return static_cast<size_t>(v ? std::max(1, std::atoi(v)) : 1);
     }();
     size_t chunks = std::min(cap, std::max<size_t>(1, w.tiles / min_tiles));
     static const size_t big_chunks = [] {  // AIDW_K4_MAX_CHUNKS: tuning only

@@ -224,8 +224,8 @@ def test_workspace_reuse_across_sizes_and_threads():
 
 @pytest.mark.parametrize("m", [2, 255, 256, 257, 2047, 2048, 2049, 4097, 262_144, 262_145])
 def test_tile_and_chunk_boundaries(m):
-    """Data sizes at the K4 tile (256), chunk-split (8 tiles per chunk, 64
-    chunks up to 1024 tiles, 16 beyond) and nearest-search grid (4096)
+    """Data sizes at the K4 tile (256), chunk-split (one tile per chunk up to
+    64 chunks, 64 chunks up to 1024 tiles, 32 beyond) and nearest-search grid (4096)
     boundaries: partial last tiles are NEAR with exact-zero pads, every
     chunk is folded once — predictions within the contract, alpha exact."""
     data = A.generate_random_points(m, UNIT, 31)
