@@ -1,6 +1,7 @@
 """Small end-to-end runs for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): the fused pipeline (FP32 and FP64 weighting, aidw and
-idw), the drop-in batch calls, the raster path and a crowded-cell grid."""
+idw), the drop-in batch calls, the raster path, a crowded-cell grid, the recipe
+classes (alpha = 1, 2, 3, 4, mixed warps) and the per-call workspace reuse."""
 import os
 import sys
 
@@ -14,6 +15,11 @@ data = A.generate_random_points(5000, UNIT, 1)
 q = A.generate_random_queries(777, UNIT, 2)
 A.run_pipeline(data, q, A.RunConfig(params=A.AidwParams(k=10)))
 A.run_pipeline(data, q, A.RunConfig(mode="idw", alpha=2.0))
+A.run_pipeline(data, q, A.RunConfig(mode="idw", alpha=1.0))
+A.run_pipeline(data, q, A.RunConfig(mode="idw", alpha=3.0))
+# recipe classes mixed with each other and with general alpha in one warp
+A.run_pipeline(A.generate_clustered(8000, seed=5), q,
+               A.RunConfig(params=A.AidwParams(k=10, alpha_levels=(1.0, 1.0, 2.0, 3.0, 4.0))))
 A.set_weight_precision("fp64")
 A.run_pipeline(data, q, A.RunConfig(params=A.AidwParams(k=15)))
 A.set_weight_precision("fp32")
