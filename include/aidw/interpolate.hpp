@@ -10,7 +10,10 @@
 // Precision contract: Variant::blocked uses the FP32 MUFU kernel
 // (|err| <= 1e-5 * max(|ref|, 1e-3 * value span) against the FP64
 // reference); Variant::naive and pinned_order use the FP64 kernel
-// (index-order sums, 1 / pow(sqrt(d2), alpha); <= 2e-11 relative).
+// (<= 2e-11 relative): index-order running sums inside each data chunk of
+// the m-only chunking (up to 64 chunks), the chunk sums then added in chunk
+// order; w = 1 / pow(sqrt(d2), alpha), or 1 / (d2 d2) for alpha == 4 —
+// not the reference's single index-order loop, but within its contract.
 // Setting AIDW_WEIGHT_FP64=1 (or aidw_set_weight_precision) routes
 // Variant::blocked to the FP64 kernel too.  Snap, nearest-value fallback
 // and hull clamp follow the reference exactly (see csrc/weight.cu).

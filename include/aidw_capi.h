@@ -73,7 +73,9 @@ enum { AIDW_MODE_IDW = 0, AIDW_MODE_AIDW = 1 };           /* cli::Mode, cli.hpp:
 
 /* Weighting precision of Variant::blocked.  FP32 (default) is the MUFU
  * kernel with the 1e-5 contract; FP64 routes blocked to the FP64 kernel
- * (index-order, pow), as Variant::naive and pinned_order always are.  The
+ * (chunk-ordered FP64 partial sums: index order within each data chunk,
+ * chunks added in order; pow, or 1 / (d2 d2) at alpha == 4), as
+ * Variant::naive and pinned_order always are.  The
  * environment variable AIDW_WEIGHT_FP64=1 sets FP64 at library load. */
 enum { AIDW_PRECISION_FP32 = 0, AIDW_PRECISION_FP64 = 1 };
 
@@ -126,6 +128,13 @@ int32_t aidw_get_weight_precision(void);
  * the general-alpha roofline separately). */
 void aidw_set_alpha4_recipe(int32_t enabled);
 
+/* Queries per weighting launch (K4 + settle).  The weighting keeps FP64
+ * partial sums of 16 B x data chunks per query in flight; the query set is
+ * processed in slabs so that memory is bounded by the slab, not by n
+ * (default 0: 2 GiB of partials, 4M queries at 32 chunks).  Rounded down to
+ * a multiple of 1024, at least 1024.  Results never depend on it. */
+void aidw_set_query_slab(int64_t queries);
+
 /* ------------------------------------------------------------ grid (K1) */
 /* build_index — grid.hpp:176-213.  sorted_ids/sorted_x/sorted_y: m entries,
  * cell_start: n_col*n_row + 1 entries (exclusive prefix). */
@@ -175,6 +184,15 @@ int aidw_idw_predict_all(const double* qx, const double* qy, size_t n, const dou
 int aidw_set_devices(const int32_t* ids, int32_t count, aidw_error* err);
 /* Number of devices the pipeline calls use (>= 1). */
 int32_t aidw_device_count(void);
+
+/* Multi-device data replication: the data arrays go host ->
+ * first listed device once, then ncclBroadcast (ncclCommInitAll over the
+ * distinct devices, cached) to the others; shards on one device share its
+ * replica.  NCCL is dlopen'ed ("libnccl.so.2"); without it CUDA peer copies
+ * fill the replicas.  Introspection for tests and logs: */
+int64_t aidw_nccl_broadcast_count(void); /* grouped broadcasts issued so far   */
+int32_t aidw_last_replication(void);     /* 0 none, 1 NCCL broadcast, 2 peer   */
+int32_t aidw_nccl_version(void);         /* NCCL_VERSION_CODE, 0 if unloadable */
 
 /* ------------------------------------------------------------ pipeline */
 /* cli::run_pipeline — cli.hpp:217-268, fused and device-resident between

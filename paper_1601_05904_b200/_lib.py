@@ -90,8 +90,12 @@ SIGNATURES = {
     "aidw_set_weight_precision": (None, [C.c_int32]),
     "aidw_get_weight_precision": (C.c_int32, []),
     "aidw_set_alpha4_recipe": (None, [C.c_int32]),
+    "aidw_set_query_slab": (None, [C.c_int64]),
     "aidw_set_devices": (C.c_int, [_i32p, C.c_int32, _ep]),
     "aidw_device_count": (C.c_int32, []),
+    "aidw_nccl_broadcast_count": (C.c_int64, []),
+    "aidw_last_replication": (C.c_int32, []),
+    "aidw_nccl_version": (C.c_int32, []),
     "aidw_build_index": (C.c_int, [_dp, _dp, C.c_size_t, C.POINTER(GridConfig), _u32p, _u32p,
                                    _dp, _dp, _ep]),
     "aidw_knn_stage": (C.c_int, [_dp, _dp, C.c_size_t, C.POINTER(GridConfig), _u32p, _u32p,

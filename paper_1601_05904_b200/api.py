@@ -202,6 +202,12 @@ def set_alpha4_recipe(enabled: bool):
     lib().aidw_set_alpha4_recipe(1 if enabled else 0)
 
 
+def set_query_slab(queries: int = 0):
+    """Queries per weighting launch (0 = default: 2 GiB of FP64 partials).
+    Bounds the weighting's memory for any n; results never depend on it."""
+    lib().aidw_set_query_slab(int(queries))
+
+
 def set_devices(ids) -> None:
     """Devices run_pipeline / run_raster spread over, one host thread each
     (query / lattice-row shards; results bit-identical to one device).
@@ -214,6 +220,15 @@ def set_devices(ids) -> None:
 
 def device_count() -> int:
     return int(lib().aidw_device_count())
+
+
+def replication_info() -> dict:
+    """How the last multi-device run replicated the data: NCCL
+    broadcasts issued so far, the last replication kind and NCCL's version."""
+    kinds = {0: "none", 1: "nccl_broadcast", 2: "peer_copy"}
+    return {"nccl_broadcasts": int(lib().aidw_nccl_broadcast_count()),
+            "last": kinds.get(int(lib().aidw_last_replication()), "?"),
+            "nccl_version": int(lib().aidw_nccl_version())}
 
 
 def kernel_launch_count():

@@ -32,6 +32,7 @@
 #include "aidw_capi.h"
 #include "common.cuh"
 #include "knn.cuh"
+#include "replicate.cuh"
 #include "weight.cuh"
 
 namespace aidwb {
@@ -472,7 +473,13 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     a.ref_candidates = candbuf.get() + 1;
     const double area = params.area > 0.0 ? params.area : ext.box.area();
     const double r_exp_arg = static_cast<double>(m) / area;
-    if (!(area > 0.0) || !std::isfinite(area))
+    // the reference's order (cli.hpp:240-259): the grid engine's cell width
+    // rejects a zero-area bbox (invalid_argument) before any query runs; the
+    // per-query area failure of aidw_predict_all needs a query to fail on
+    aidw_grid_config gc{};
+    if (cfg.engine == AIDW_ENGINE_GRID)
+        gc = make_grid_config_h(ext.box, choose_cell_width_h(m, ext.box, cfg.cell_factor));
+    if (n > 0 && (!(area > 0.0) || !std::isfinite(area)))
         throw Failure(AIDW_ERR_RUNTIME,
                       "aidw_predict_all: query 0: expected_nn_distance: area must be positive finite", 0);
     const double r_exp = 1.0 / (2.0 * std::sqrt(r_exp_arg));  // adaptive.hpp:27
@@ -493,8 +500,6 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
 
     DeviceGrid g;  // lives until the weighting stage has read its cell order
     if (cfg.engine == AIDW_ENGINE_GRID) {
-        const double width = choose_cell_width_h(m, ext.box, cfg.cell_factor);
-        const aidw_grid_config gc = make_grid_config_h(ext.box, width);
         validate_params(params);
         CK(cudaEventRecord(e_build0, s));
         build_grid_device(io.dx, io.dy, m, gc, g, fails.slot(kFailData), s);
@@ -732,15 +737,32 @@ std::vector<int> device_list() {
     return g_devices;
 }
 
-// One shard's device buffers (released on the shard's own thread).
+// One shard's device buffers (released on the shard's own thread); the
+// data arrays are its device's replica (shared by the shards on a device).
 struct ShardBufs {
-    DBuf<double> dx, dy, dz, qx, qy, pred, alpha;
+    const double *dx = nullptr, *dy = nullptr, *dz = nullptr;
+    DBuf<double> qx, qy, pred, alpha;
     double h2d_ms = 0.0;
     void release() {
-        dx.release(), dy.release(), dz.release(), qx.release(), qy.release();
+        qx.release(), qy.release();
         pred.release(), alpha.release();
     }
 };
+
+// The data set on every listed device: one H2D to the first, ncclBroadcast
+// to the others (replicate.cu); each shard points at its device's replica.
+double replicate_for_shards(const std::vector<int>& devs, const double* dx, const double* dy,
+                            const double* dz, size_t m, Replicas& reps, ShardBufs* b) {
+    const auto c0 = std::chrono::steady_clock::now();
+    replicate_data(devs, dx, dy, dz, m, reps);
+    for (size_t d = 0; d < devs.size(); ++d) {
+        const int r = reps.slot_of(devs[d]);
+        b[d].dx = reps.x[r];
+        b[d].dy = reps.y[r];
+        b[d].dz = reps.z[r];
+    }
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+}
 
 // A reusable-free count-down barrier for the shard threads.
 struct ShardBarrier {
@@ -866,16 +888,13 @@ struct PipelineShards {
         size_t lo, hi;
         shard_bounds(n, D, d, lo, hi);
         const auto c0 = std::chrono::steady_clock::now();
-        h2d(b[d].dx, dx, m, s);
-        h2d(b[d].dy, dy, m, s);
-        h2d(b[d].dz, dz, m, s);
         h2d(b[d].qx, qx + lo, hi - lo, s);
         h2d(b[d].qy, qy + lo, hi - lo, s);
         b[d].pred.alloc(hi - lo, s);
         b[d].alpha.alloc(hi - lo, s);
         const Extents e =
-            extents(b[d].dx.get(), b[d].dy.get(), m, b[d].qx.get(), b[d].qy.get(), hi - lo, nullptr, 0, s);
-        b[d].h2d_ms =
+            extents(b[d].dx, b[d].dy, m, b[d].qx.get(), b[d].qy.get(), hi - lo, nullptr, 0, s);
+        b[d].h2d_ms +=
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
         return e.box;
     }
@@ -890,7 +909,7 @@ struct PipelineShards {
             c.bbox[2] = g.max_x;
             c.bbox[3] = g.max_y;
         }
-        PipelineIO io{b[d].dx.get(), b[d].dy.get(), b[d].dz.get(), b[d].qx.get(), b[d].qy.get(),
+        PipelineIO io{b[d].dx, b[d].dy, b[d].dz, b[d].qx.get(), b[d].qy.get(),
                       m, hi - lo, b[d].pred.get(), b[d].alpha.get()};
         pipeline_entry(io, c, &st[d], s, b[d].h2d_ms, t0, pred_out + lo,
                        alpha_out ? alpha_out + lo : nullptr);
@@ -904,6 +923,9 @@ bool pipeline_multi(const std::vector<int>& devs, const double* dx, const double
     const size_t D = devs.size();
     std::unique_ptr<ShardBufs[]> bufs(new ShardBufs[D]);
     std::unique_ptr<aidw_run_stats[]> st(new aidw_run_stats[D]());
+    Replicas reps;
+    const double rep_ms = replicate_for_shards(devs, dx, dy, dz, m, reps, bufs.get());
+    for (size_t d = 0; d < D; ++d) bufs[d].h2d_ms = rep_ms;
     PipelineShards job{dx, dy, dz, qx, qy, m, n, D, cfg, pred_out, alpha_out, t0, bufs.get(), st.get()};
     PipelineShards* j = &job;
     ShardBufs* b = bufs.get();
@@ -926,13 +948,7 @@ struct RasterShards {
     aidw_run_stats* st;
 
     Box prep(size_t d, cudaStream_t s) {
-        const auto c0 = std::chrono::steady_clock::now();
-        h2d(b[d].dx, dx, m, s);
-        h2d(b[d].dy, dy, m, s);
-        h2d(b[d].dz, dz, m, s);
-        const Extents e = extents(b[d].dx.get(), b[d].dy.get(), m, nullptr, nullptr, 0, nullptr, 0, s);
-        b[d].h2d_ms =
-            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+        const Extents e = extents(b[d].dx, b[d].dy, m, nullptr, nullptr, 0, nullptr, 0, s);
         return e.box;
     }
     void run(size_t d, cudaStream_t s, const Box& g) {
@@ -948,7 +964,7 @@ struct RasterShards {
         aidw_run_config c = cfg;
         c.use_bbox = 1;
         std::memcpy(c.bbox, bb, sizeof bb);
-        PipelineIO io{b[d].dx.get(), b[d].dy.get(), b[d].dz.get(), b[d].qx.get(), b[d].qy.get(),
+        PipelineIO io{b[d].dx, b[d].dy, b[d].dz, b[d].qx.get(), b[d].qy.get(),
                       m, n, b[d].pred.get(), b[d].alpha.get()};
         pipeline_entry(io, c, &st[d], s, b[d].h2d_ms, t0, raster_out + nx * r0,
                        alpha_out ? alpha_out + nx * r0 : nullptr);
@@ -963,6 +979,9 @@ bool raster_multi(const std::vector<int>& devs, const double* dx, const double* 
     std::unique_ptr<ShardBufs[]> bufs(new ShardBufs[D]);
     std::unique_ptr<aidw_run_stats[]> st(new aidw_run_stats[D]());
     std::unique_ptr<Box[]> box(new Box[1]);
+    Replicas reps;
+    const double rep_ms = replicate_for_shards(devs, dx, dy, dz, m, reps, bufs.get());
+    for (size_t d = 0; d < D; ++d) bufs[d].h2d_ms = rep_ms;
     RasterShards job{dx, dy, dz, m, nx, ny, D, cfg, raster_out, alpha_out, t0, bufs.get(), st.get()};
     RasterShards* j = &job;
     ShardBufs* b = bufs.get();
@@ -1004,6 +1023,8 @@ void aidw_set_weight_precision(int32_t precision) {
 int32_t aidw_get_weight_precision(void) { return g_precision.load(); }
 
 void aidw_set_alpha4_recipe(int32_t enabled) { set_alpha4_recipe(enabled != 0); }
+
+void aidw_set_query_slab(int64_t queries) { set_query_slab(queries > 0 ? static_cast<size_t>(queries) : 0); }
 
 int aidw_device_info(char* name, size_t cap, int32_t* sm_count, aidw_error* err) {
     return guarded(err, [&] {
@@ -1254,6 +1275,10 @@ int32_t aidw_device_count(void) {
     const auto d = device_list();
     return static_cast<int32_t>(d.size() > 1 ? d.size() : 1);
 }
+
+int64_t aidw_nccl_broadcast_count(void) { return nccl_broadcast_count(); }
+int32_t aidw_last_replication(void) { return last_replication_kind(); }
+int32_t aidw_nccl_version(void) { return nccl_version(); }
 
 int aidw_run_pipeline(const double* dx, const double* dy, const double* dz, size_t m,
                       const double* qx, const double* qy, size_t n, const aidw_run_config* cfg,

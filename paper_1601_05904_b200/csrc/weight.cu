@@ -403,7 +403,8 @@ struct K4Args {
     size_t n;
     const uint32_t* flag_a;  // class counts: A = scan_a[n-1] + flag_a[n-1]
     const uint32_t* scan_a;
-    double2* part;            // chunks x n (chunk-major: coalesced), by visiting position
+    size_t s0, s1;            // this launch's query slab [s0, s1) of the visiting order
+    double2* part;            // chunks x (s1 - s0) (chunk-major: coalesced), by position - s0
     const float4* tile_box;   // hi-coordinate box of every tile's real records
     const float4* tile_geo;   // {cx, cy, near threshold^2, 0}
 };
@@ -965,15 +966,18 @@ __device__ __forceinline__ void k4_body(const K4Args& a, size_t q0, size_t q1, s
 #pragma unroll
     for (int i = 0; i < kQT; ++i) {
         const size_t p = wbase + static_cast<size_t>(i) * 32 + lane;
-        if (p < q1) a.part[static_cast<size_t>(chunk) * a.n + p] = make_double2(SW[i], SWZ[i]);
+        if (p < q1)
+            a.part[static_cast<size_t>(chunk) * (a.s1 - a.s0) + (p - a.s0)] = make_double2(SW[i], SWZ[i]);
     }
 }
 
-// One launch for both classes: CTAs [0, ceil(nG / Q)) take the general
-// region [0, nG) of the visiting order, the rest the recipe region [nG, n)
-// (Q = queries per CTA).  The class counts live on the device (no host sync
-// mid-pipeline); the grid is sized for ceil(n / Q) + 1 CTAs, any surplus
-// CTA exits at once.
+// One launch for both classes of a query slab [s0, s1): CTAs
+// [0, ceil(|G| / Q)) take G = [s0, s1) ∩ [0, nG), the general region of the
+// visiting order, the rest R = [s0, s1) ∩ [nG, n), the recipe region
+// (Q = queries per CTA; s0 is a multiple of Q, so G keeps the warp-aligned
+// G1 / G2 interleave).  The class counts live on the device (no host sync
+// mid-pipeline); the grid is sized for ceil((s1 - s0) / Q) + 1 CTAs, any
+// surplus CTA exits at once.
 template <int kQT, int kMinBlocks>
 __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -983,9 +987,11 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
     constexpr size_t kQ = static_cast<size_t>(kK4Threads) * kQT;
     const size_t num_a = static_cast<size_t>(a.scan_a[a.n - 1]) + a.flag_a[a.n - 1];
     const size_t num_g = a.n - num_a;
-    const size_t ctas_g = (num_g + kQ - 1) / kQ;
+    const size_t g0 = a.s0, g1 = a.s1 < num_g ? a.s1 : num_g;
+    const size_t r0 = a.s0 > num_g ? a.s0 : num_g, r1 = a.s1;
+    const size_t ctas_g = g1 > g0 ? (g1 - g0 + kQ - 1) / kQ : 0;
     const size_t b = blockIdx.x;
-    if (b >= ctas_g && (b - ctas_g) * kQ >= num_a) return;
+    if (b >= ctas_g && (r1 <= r0 || (b - ctas_g) * kQ >= r1 - r0)) return;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&bar[s], 1);
@@ -994,8 +1000,8 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
         fence_mbar_init();
     }
     __syncthreads();
-    if (b < ctas_g) k4_body<false, kQT>(a, 0, num_g, b, stile, bar, done);
-    else k4_body<true, kQT>(a, num_g, a.n, b - ctas_g, stile, bar, done);
+    if (b < ctas_g) k4_body<false, kQT>(a, g0, g1, b, stile, bar, done);
+    else k4_body<true, kQT>(a, r0, r1, b - ctas_g, stile, bar, done);
 }
 
 // ------------------------------------------------------------ settle
@@ -1003,9 +1009,10 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
                               const uint32_t* __restrict__ order,
                               const double2* __restrict__ part,
                               const double* __restrict__ lshift, unsigned chunks,
-                              double* __restrict__ pred, double* __restrict__ alpha_out) {
-    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= q.n) return;
+                              size_t s0, size_t s1, double* __restrict__ pred,
+                              double* __restrict__ alpha_out) {
+    const size_t i = s0 + static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= s1) return;
     const uint32_t p = order[i];
     const uint32_t qi = q.perm ? q.perm[p] : p;
     const double alpha = q.alpha_s[p];
@@ -1016,7 +1023,7 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
     } else {
         double sw = 0.0, swz = 0.0;
         for (unsigned c = 0; c < chunks; ++c) {
-            const double2 v = part[static_cast<size_t>(c) * q.n + i];
+            const double2 v = part[static_cast<size_t>(c) * (s1 - s0) + (i - s0)];
             sw += v.x;
             swz += v.y;
         }
@@ -1042,6 +1049,21 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
 }  // namespace
 
 void set_alpha4_recipe(bool enabled) { g_alpha4_recipe.store(enabled); }
+
+namespace {
+std::atomic<size_t> g_query_slab{0};
+}
+
+void set_query_slab(size_t queries) { g_query_slab.store(queries); }
+
+size_t query_slab(unsigned chunks) {
+    // default: 2 GiB of FP64 partials (4M queries at 32 data chunks, 2M at
+    // 64); a multiple of 1024 so every slab starts on a K4 CTA boundary
+    size_t v = g_query_slab.load();
+    if (v == 0) v = (size_t(2) << 30) / (16 * static_cast<size_t>(chunks ? chunks : 1));
+    v = std::max<size_t>(1024, v & ~size_t(1023));
+    return v;
+}
 
 WeightSplit weight_split(size_t m) {
     // Data chunks per query (the grid's y dimension): enough CTAs to fill
@@ -1132,9 +1154,12 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
            flag.get(), scan_a.get(), rf, flag_g2.get(), scan_g2.get(), order_q.get(), qhl.get(), qpar.get(),
            lshift.get(), times ? times->d_alpha4 : nullptr);
 
-    DBuf<double2> part(q.n * sp.chunks, s);
+    // queries in slabs: the FP64 partials (16 B x chunks per query) are
+    // bounded by the slab, not by n; per-query results never depend on it
+    const size_t slab = std::min(q.n, query_slab(sp.chunks));
+    DBuf<double2> part(slab * sp.chunks, s);
     K4Args ka{rec.get(), sp.tiles, sp.tiles_per_chunk, sp.chunks, qhl.get(), qpar.get(),
-              q.n, flag.get(), scan_a.get(), part.get(), tbox.get(), tgeo.get()};
+              q.n, flag.get(), scan_a.get(), 0, 0, part.get(), tbox.get(), tgeo.get()};
     const size_t smem = kStages * kTileFloats * sizeof(float) + kStages * sizeof(uint64_t) +
                         kStages * sizeof(unsigned);
     // K4 variant: queries per thread x min resident CTAs (AIDW_K4_VARIANT for
@@ -1147,26 +1172,32 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     auto launch = [&](auto kernel, int qt) {
         CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-        dim3 grid(ceil_div(q.n, static_cast<size_t>(kK4Threads) * qt) + 1, sp.chunks);
-        if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+        dim3 grid(ceil_div(ka.s1 - ka.s0, static_cast<size_t>(kK4Threads) * qt) + 1, sp.chunks);
         LAUNCH(kernel, grid, kK4Threads, smem, s, ka);
     };
     // Few queries for the data size (n / 1024 x chunks CTAs short of ~16
     // waves of 148 x 2): 2 queries per thread, 4 CTAs / SM — twice the CTAs
     // (e.g. 20K queries x 20M points: 369 -> 215 ms).  The per-query
     // arithmetic is the same in every launch shape.
-    const size_t ctas4 = ceil_div(q.n, static_cast<size_t>(kK4Threads) * 4) * sp.chunks;
+    const size_t ctas4 = ceil_div(slab, static_cast<size_t>(kK4Threads) * 4) * sp.chunks;
     const int shape = variant != 0 ? variant : (ctas4 < static_cast<size_t>(16 * 148 * 2) ? 2 : 0);
-    switch (shape) {
-        case 1: launch(weight_fp32_kernel<4, 3>, 4); break;
-        case 2: launch(weight_fp32_kernel<2, 4>, 2); break;
-        case 3: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;
-        case 4: launch(weight_fp32_kernel<2, 3>, 2); break;
-        default: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;
+    // (with several slabs the K4 events also bracket the settles between
+    // them: ~1e-4 of a K4 slab)
+    if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+    for (size_t s0 = 0; s0 < q.n; s0 += slab) {
+        ka.s0 = s0;
+        ka.s1 = std::min(q.n, s0 + slab);
+        switch (shape) {
+            case 1: launch(weight_fp32_kernel<4, 3>, 4); break;
+            case 2: launch(weight_fp32_kernel<2, 4>, 2); break;
+            case 3: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;
+            case 4: launch(weight_fp32_kernel<2, 3>, 2); break;
+            default: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;
+        }
+        if (times && times->k4_end && ka.s1 == q.n) CK(cudaEventRecord(times->k4_end, s));
+        LAUNCH(settle_kernel, ceil_div(ka.s1 - ka.s0, kThreads), kThreads, 0, s, q, f, d,
+               order_q.get(), part.get(), lshift.get(), sp.chunks, ka.s0, ka.s1, d_pred, d_alpha);
     }
-    if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
-    LAUNCH(settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order_q.get(),
-           part.get(), lshift.get(), sp.chunks, d_pred, d_alpha);
 }
 
 }  // namespace aidwb

@@ -59,7 +59,9 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
                     double* d_pred, double* d_alpha, WeightTimes* times, cudaStream_t s);
 
 // FP64 path (Variant::naive, pinned_order, AIDW_WEIGHT_FP64): index-order
-// accumulation with 1 / pow(sqrt(d2), alpha), reference snap / fallback.
+// accumulation inside each data chunk (chunking a function of m), chunk sums
+// added in chunk order; 1 / pow(sqrt(d2), alpha) (1 / (d2 d2) at alpha = 4),
+// reference snap / fallback.
 // `blocked` selects the reference's blocked-variant arithmetic (recipe /
 // exp-log, chunked sums) instead of the naive pow form.
 void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFrame& f,
@@ -78,5 +80,11 @@ constexpr int kWeightTile = 256;
 
 // Global switch of the alpha == 4 one-MUFU recipe (aidw_set_alpha4_recipe).
 void set_alpha4_recipe(bool enabled);
+
+// Queries per weighting launch (K4 + settle): bounds the FP64 partial sums
+// to slab x chunks x 16 B whatever n is (aidw_set_query_slab; 0 = default,
+// 2 GiB of partials).  Always a multiple of 1024.
+void set_query_slab(size_t queries);
+size_t query_slab(unsigned chunks);
 
 }  // namespace aidwb

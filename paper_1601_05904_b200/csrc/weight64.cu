@@ -1,8 +1,12 @@
 // weight64.cu — the FP64 weighting kernels.
 //
 //  NAIVE   (Variant::naive, pinned_order): restates predict_naive + settle
-//          (proj/include/aidw/interpolate.hpp:94-137): w = 1/pow(sqrt(d2), a),
-//          sums in index order.
+//          (proj/include/aidw/interpolate.hpp:94-137): w = 1/pow(sqrt(d2), a)
+//          (1 / (d2 d2) to ~1 ulp when a == 4); running sums in index order
+//          within each data chunk (up to 64, a function of m), the chunk sums
+//          added in chunk order by fp64_settle_kernel — so the summation
+//          order is chunk-ordered, not the reference's single index-order
+//          loop (within the 2e-11 contract).
 //  BLOCKED (Variant::blocked under AIDW_WEIGHT_FP64): restates the scalar
 //          semantics of predict_blocked_fast (:168-209, :252-381): the exact
 //          half-integer recipe d2^(n/4) via products and square roots when
@@ -18,6 +22,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -98,20 +103,21 @@ template <bool BLOCKED, int QT>
 __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQueries q,
                                                           const WeightData d,
                                                           const uint32_t* __restrict__ order,
-                                                          size_t chunk_pts,
+                                                          size_t chunk_pts, size_t s0,
+                                                          size_t s1,
                                                           double2* __restrict__ part) {
     __shared__ double2 sxy[kTile64];
     __shared__ double sz[kTile64];
-    const size_t p0 = static_cast<size_t>(blockIdx.x) * blockDim.x * QT + threadIdx.x;
+    const size_t p0 = s0 + static_cast<size_t>(blockIdx.x) * blockDim.x * QT + threadIdx.x;
     double qx[QT], qy[QT], alpha[QT], e[QT], sw[QT], swz[QT];
     int n4[QT];
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
         const size_t slot = p0 + static_cast<size_t>(i) * blockDim.x;
-        const size_t p = slot < q.n ? order[slot] : slot;
+        const size_t p = slot < s1 ? order[slot] : slot;
         qx[i] = qy[i] = 0.0;
         alpha[i] = 4.0;
-        if (slot < q.n) {
+        if (slot < s1) {
             const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
             qx[i] = q.qx[qi];
             qy[i] = q.qy[qi];
@@ -148,7 +154,10 @@ __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQ
 #pragma unroll
                 for (int i = 0; i < QT; ++i) {
                     const double d2 = dsq_rn(qx[i], qy[i], xy.x, xy.y);
-                    const double w = rcp_nr(__dmul_rn(d2, d2));
+                    // d2^2 overflowing to inf weighs 0, as 1 / pow(sqrt(d2), 4)
+                    // does in the reference (rcp_nr(inf) would give NaN)
+                    const double a4 = __dmul_rn(d2, d2);
+                    const double w = a4 < INFINITY ? rcp_nr(a4) : 0.0;
                     if (BLOCKED) {
                         cw[i] = __dadd_rn(cw[i], w);
                         cwz[i] = __dadd_rn(cwz[i], __dmul_rn(w, z));
@@ -188,7 +197,8 @@ __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQ
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
         const size_t slot = p0 + static_cast<size_t>(i) * blockDim.x;
-        if (slot < q.n) part[static_cast<size_t>(blockIdx.y) * q.n + slot] = make_double2(sw[i], swz[i]);
+        if (slot < s1)
+            part[static_cast<size_t>(blockIdx.y) * (s1 - s0) + (slot - s0)] = make_double2(sw[i], swz[i]);
     }
 }
 
@@ -199,9 +209,10 @@ __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQ
 __global__ void fp64_settle_kernel(const WeightQueries q, const WeightFrame f, const WeightData d,
                                    const uint32_t* __restrict__ order,
                                    const double2* __restrict__ part, unsigned chunks,
-                                   double* __restrict__ pred, double* __restrict__ alpha_out) {
-    const size_t slot = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (slot >= q.n) return;
+                                   size_t s0, size_t s1, double* __restrict__ pred,
+                                   double* __restrict__ alpha_out) {
+    const size_t slot = s0 + static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (slot >= s1) return;
     const size_t p = order[slot];
     const uint32_t qi = q.perm ? q.perm[p] : static_cast<uint32_t>(p);
     double out;
@@ -211,7 +222,7 @@ __global__ void fp64_settle_kernel(const WeightQueries q, const WeightFrame f, c
     } else {
         double sw = 0.0, swz = 0.0;
         for (unsigned c = 0; c < chunks; ++c) {
-            const double2 v = part[static_cast<size_t>(c) * q.n + slot];
+            const double2 v = part[static_cast<size_t>(c) * (s1 - s0) + (slot - s0)];
             sw = __dadd_rn(sw, v.x);
             swz = __dadd_rn(swz, v.y);
         }
@@ -258,24 +269,30 @@ void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFra
     const WeightSplit sp = weight_split(d.m);
     const size_t chunk_pts = sp.tiles_per_chunk * static_cast<size_t>(kWeightTile);
     const unsigned chunks = static_cast<unsigned>((d.m + chunk_pts - 1) / chunk_pts);
-    DBuf<double2> part(static_cast<size_t>(chunks) * q.n, s);
+    // queries in slabs (see query_slab): partials bounded whatever n is
+    const size_t slab = std::min(q.n, query_slab(chunks));
+    DBuf<double2> part(static_cast<size_t>(chunks) * slab, s);
+    size_t s0 = 0, s1 = 0;
     auto go = [&](auto kernel, int k) {
-        if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
-        const dim3 grid(ceil_div(q.n, static_cast<size_t>(kFp64Threads * k)), chunks);
-        LAUNCH(kernel, grid, kFp64Threads, 0, s, q, d, order.get(), chunk_pts, part.get());
+        const dim3 grid(ceil_div(s1 - s0, static_cast<size_t>(kFp64Threads * k)), chunks);
+        LAUNCH(kernel, grid, kFp64Threads, 0, s, q, d, order.get(), chunk_pts, s0, s1, part.get());
     };
-    if (blocked) {
-        if (qt == 4) go(weight_fp64_kernel<true, 4>, 4);
-        else if (qt == 2) go(weight_fp64_kernel<true, 2>, 2);
-        else go(weight_fp64_kernel<true, 1>, 1);
-    } else {
-        if (qt == 4) go(weight_fp64_kernel<false, 4>, 4);
-        else if (qt == 2) go(weight_fp64_kernel<false, 2>, 2);
-        else go(weight_fp64_kernel<false, 1>, 1);
+    if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+    for (s0 = 0; s0 < q.n; s0 += slab) {
+        s1 = std::min(q.n, s0 + slab);
+        if (blocked) {
+            if (qt == 4) go(weight_fp64_kernel<true, 4>, 4);
+            else if (qt == 2) go(weight_fp64_kernel<true, 2>, 2);
+            else go(weight_fp64_kernel<true, 1>, 1);
+        } else {
+            if (qt == 4) go(weight_fp64_kernel<false, 4>, 4);
+            else if (qt == 2) go(weight_fp64_kernel<false, 2>, 2);
+            else go(weight_fp64_kernel<false, 1>, 1);
+        }
+        if (times && times->k4_end && s1 == q.n) CK(cudaEventRecord(times->k4_end, s));
+        LAUNCH(fp64_settle_kernel, ceil_div(s1 - s0, kThreads), kThreads, 0, s, q, f, d,
+               order.get(), part.get(), chunks, s0, s1, d_pred, d_alpha);
     }
-    if (times && times->k4_end) CK(cudaEventRecord(times->k4_end, s));
-    LAUNCH(fp64_settle_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, d, order.get(),
-           part.get(), chunks, d_pred, d_alpha);
 }
 
 }  // namespace aidwb

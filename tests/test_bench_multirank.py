@@ -28,11 +28,16 @@ def torchrun(port, *args):
 @pytest.mark.gpu
 def test_two_rank_bench_line():
     b = torchrun(29531, "--config", "100k", "--steps", "2", "--warmup", "3",
-                 "--no-cpu-baseline")
-    assert b["n_gpus"] == 2 and b["scaling"] == "weak"
+                 "--no-cpu-baseline", "--no-fp64")
+    # configs as written: the 100K queries sharded over the 2 ranks (strong)
+    assert b["n_gpus"] == 2 and b["scaling"] == "strong"
+    assert b["config"]["n"] == 100_000 and b["hardware"]["per_rank_queries"] == 50_000
     assert b["value"] > 0 and b["e2e"]["value"] > 0
-    assert abs(b["value"] - 2 * 100_000 / (b["ms_per_step"] / 1e3)) <= 1e-6 * b["value"]
+    assert abs(b["value"] - 100_000 / (b["ms_per_step"] / 1e3)) <= 1e-6 * b["value"]
     assert b["gpu_launches"] > 0
+    # the weak-scaling figure beside it: 100K queries per rank
+    w = b["weak_scaling"]
+    assert w["n"] == 200_000 and w["per_rank"] == 100_000 and w["value"] > 0
 
 
 @pytest.mark.gpu
@@ -40,3 +45,6 @@ def test_two_rank_reference_arm():
     b = torchrun(29532, "--impl", "reference", "--config", "100k", "--steps", "1",
                  "--warmup", "1")
     assert b["impl"] == "reference" and b["value"] > 0
+    # the reference arm never maps the repo's library
+    assert b["config"]["n"] == 100_000 and b["scaling"] == "strong"
+    assert b["repo_library_mapped"] is False

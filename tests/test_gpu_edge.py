@@ -235,3 +235,45 @@ def test_tile_and_chunk_boundaries(m):
     ref = O.pipeline(data.xs, data.ys, data.zs, q.xs, q.ys, k=k, variant=1)
     assert np.max(np.abs(out.result.alphas - ref["alpha"]) / ref["alpha"]) <= 1e-12
     assert pred_err(out.result.predicted, ref["pred"], data.zs) <= 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_query_slabs_bit_identical(precision):
+    """The weighting runs its queries in slabs (aidw_set_query_slab) so its
+    FP64 partial sums are bounded for any n: 3 / 1 KiB-query slabs give the
+    bits of one slab, for AIDW (both query classes, general and alpha = 4
+    regions straddling slab boundaries) and constant-alpha IDW."""
+    data = A.generate_clustered(60_000, seed=3)
+    q = A.generate_random_queries(10_000, UNIT, 4)
+    A.set_weight_precision(precision)
+    cfg = A.RunConfig(params=A.AidwParams(k=10))
+    icfg = A.RunConfig(mode="idw", alpha=2.5)
+    try:
+        A.set_query_slab(0)
+        ref = A.run_pipeline(data, q, cfg).result
+        ref_idw = A.run_pipeline(data, q, icfg).result
+        for slab in (3072, 1024):
+            A.set_query_slab(slab)
+            got = A.run_pipeline(data, q, cfg).result
+            assert np.array_equal(got.predicted, ref.predicted)
+            assert np.array_equal(got.alphas, ref.alphas)
+            assert np.array_equal(A.run_pipeline(data, q, icfg).result.predicted, ref_idw.predicted)
+    finally:
+        A.set_query_slab(0)
+    assert 0.05 < np.mean(ref.alphas == 4.0) < 0.95  # both K4 regions populated
+
+
+def test_empty_queries_and_zero_area():
+    """run_pipeline with n = 0 returns empty results (brute engine too);
+    a zero-area bbox fails in the grid engine's cell width
+    (choose_cell_width, invalid_argument) as in the reference (cli.hpp:240-248)."""
+    data = A.generate_random_points(500, UNIT, 5)
+    for engine in ("grid", "brute"):
+        out = A.run_pipeline(data, A.PointSet(), A.RunConfig(knn_engine=engine))
+        assert out.result.predicted.size == 0
+    line = A.PointSet(np.linspace(0, 1, 50), np.full(50, 0.5), np.arange(50.0))
+    with pytest.raises(A.InvalidArgument) as e:
+        A.run_pipeline(line, A.PointSet([0.5], [0.5]), A.RunConfig())
+    assert "choose_cell_width" in str(e.value)
+    with pytest.raises(A.InvalidArgument):
+        A.run_pipeline(line, A.PointSet(), A.RunConfig())

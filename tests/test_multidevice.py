@@ -42,7 +42,13 @@ def test_pipeline_shards_bit_identical(shards, mode, precision):
     A.set_weight_precision(precision)
     cfg = A.RunConfig(mode=mode, params=A.AidwParams(k=10), alpha=2.5)
     assert A.device_count() == 3
+    b0 = A.replication_info()["nccl_broadcasts"]
     multi = A.run_pipeline(data, q, cfg)
+    # data replicated by NCCL: one H2D, one grouped ncclBroadcast over the
+    # distinct devices (here one; the three shards share its replica)
+    info = A.replication_info()
+    assert info["last"] == "nccl_broadcast" and info["nccl_broadcasts"] == b0 + 1
+    assert info["nccl_version"] >= 21800
     one = single(lambda: A.run_pipeline(data, q, cfg))
     assert np.array_equal(multi.result.predicted, one.result.predicted)
     assert np.array_equal(multi.result.alphas, one.result.alphas)
