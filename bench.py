@@ -254,6 +254,12 @@ class LibGen:
         return q.xs, q.ys
 
 
+def lib_inputs(A, cfg):
+    """One-rank inputs as the repo's PointSets (tools / studies)."""
+    (dx, dy, dz), (qx, qy) = make_inputs(LibGen(A), cfg, 1, 0, "strong")
+    return A.PointSet(dx, dy, dz), A.PointSet(qx, qy)
+
+
 def reference_pass(O, cfg, data, queries, stride=1, workers=0):
     """One reference cli::run_pipeline over every `stride`-th query (all the
     data): returns (wall seconds, queries interpolated, stage timings ms)."""

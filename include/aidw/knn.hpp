@@ -17,8 +17,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstddef>
+#include <condition_variable>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -184,8 +186,110 @@ inline KnnResult grid_knn(const QueryPoint& q, const GridIndex& index, int k) {
     return std::move(buf).finalize(start.exhausted);
 }
 
-/// Batch kNN stage on the GPU (aidw_knn_stage).  Output order = input
-/// order; `workers` / `chunk` are accepted and ignored (no CPU threading).
+namespace detail {
+
+/// Host-side result storage of knn_stage: n KnnResult objects whose
+/// distances_sq vectors already hold k elements.  Building them is pure host
+/// work dominated by first-touch page faults of the fresh heap (~2-3 ms per
+/// 100K results), so a background thread builds the next call's storage
+/// after each call — sized by the largest request seen, doubled (like a
+/// vector's capacity), capped at 64 MiB — and a call with a matching k takes
+/// it with no allocation.  Otherwise the storage is built on the host pool
+/// while the device runs the stage.
+class ResultStash {
+public:
+    static ResultStash& instance() {
+        static ResultStash stash;
+        return stash;
+    }
+
+    /// n results with distances_sq.size() == k.
+    std::vector<KnnResult> take(std::size_t n, std::size_t k) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (ready_ && k_ == k && stash_.size() >= n) {
+                std::vector<KnnResult> v = std::move(stash_);
+                stash_.clear();
+                ready_ = false;
+                v.resize(n);
+                return v;
+            }
+        }
+        return build(n, k);
+    }
+
+    /// Schedule the next storage after a call of shape (n, k).
+    void refill(std::size_t n, std::size_t k) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (k != k_) {
+            stash_.clear();
+            ready_ = false;
+            k_ = k;
+            want_ = 0;
+        }
+        want_ = std::max(want_, 2 * n);
+        const std::size_t per = sizeof(KnnResult) + k * sizeof(double) + 16;
+        want_ = std::min<std::size_t>(want_, (std::size_t(64) << 20) / per);
+        if (ready_ && stash_.size() >= want_) return;
+        pending_ = true;
+        cv_.notify_one();
+    }
+
+    ~ResultStash() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_one();
+        if (worker_.joinable()) worker_.join();
+    }
+
+private:
+    ResultStash() : worker_([this] { loop(); }) {}
+
+    static std::vector<KnnResult> build(std::size_t n, std::size_t k) {
+        std::vector<KnnResult> v(n);
+        HostPool::instance().parallel_for(n, 4096, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t i = lo; i < hi; ++i) v[i].distances_sq.resize(k);
+        });
+        return v;
+    }
+
+    void loop() {
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || pending_; });
+            if (stop_) return;
+            pending_ = false;
+            const std::size_t n = want_, k = k_;
+            lk.unlock();
+            std::vector<KnnResult> v(n);  // serial: never holds the host pool
+            for (KnnResult& r : v) r.distances_sq.resize(k);
+            lk.lock();
+            if (k == k_ && n >= stash_.size()) {
+                stash_ = std::move(v);
+                ready_ = true;
+            }
+        }
+    }
+
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::vector<KnnResult> stash_;
+    std::size_t k_ = 0, want_ = 0;
+    bool ready_ = false, pending_ = false, stop_ = false;
+    std::thread worker_;
+};
+
+}  // namespace detail
+
+/// Batch kNN stage on the GPU.  Output order = input order; `workers` /
+/// `chunk` are accepted and ignored (no CPU threading).  The grid engine on
+/// an index from build_index runs on its device mirror
+/// (aidw_knn_stage_mirror: only the queries are uploaded); otherwise
+/// aidw_knn_stage uploads the index arrays.  The squared distances come back
+/// into page-locked staging (aidw_pinned_alloc) and are materialised into
+/// the n KnnResult vectors on all host threads.
 inline std::vector<KnnResult> knn_stage(const PointSet& queries, const GridIndex* index,
                                         const PointSet& data, int k, KnnEngine engine,
                                         int workers = 1, std::size_t chunk = 64) {
@@ -200,52 +304,69 @@ inline std::vector<KnnResult> knn_stage(const PointSet& queries, const GridIndex
     const std::size_t k_alloc =
         k < 1 ? 0 : (grid ? std::min<std::size_t>(static_cast<std::size_t>(k), m)
                           : static_cast<std::size_t>(k));
-    // Flat staging rows, first touched in parallel (page faults of a fresh
-    // n * k buffer are most of a first call's host time at 100K queries).
-    const std::size_t threads =
-        std::min<std::size_t>(static_cast<std::size_t>(resolve_workers(0)), n / 8192 + 1);
-    auto parallel = [threads, n](auto&& body) {
-        if (threads <= 1) {
-            body(std::size_t{0}, n);
-            return;
+    // n * k_eff distances: pinned staging (full-speed D2H, no first-touch
+    // page faults), pageable if none is available
+    struct Staging {
+        double* p = nullptr;
+        bool pinned = false;
+        explicit Staging(std::size_t count) {
+            p = static_cast<double*>(aidw_pinned_alloc((count + 1) * sizeof(double)));
+            pinned = p != nullptr;
+            if (!pinned) p = new double[count + 1];
         }
-        std::vector<std::thread> pool;
-        const std::size_t step = (n + threads - 1) / threads;
-        for (std::size_t t = 0; t < threads; ++t) {
-            pool.emplace_back(body, std::min(n, t * step), std::min(n, (t + 1) * step));
+        ~Staging() {
+            if (pinned) aidw_pinned_free(p);
+            else delete[] p;
         }
-        for (auto& th : pool) th.join();
-    };
-    std::unique_ptr<double[]> d2(new double[n * k_alloc + 1]);
+        Staging(const Staging&) = delete;
+        Staging& operator=(const Staging&) = delete;
+    } d2(n * k_alloc);
     std::vector<double> avg(n);
-    parallel([&](std::size_t lo, std::size_t hi) {
-        std::fill(d2.get() + lo * k_alloc, d2.get() + hi * k_alloc, 0.0);
-    });
     int32_t k_eff = 0, exhausted = 0;
     aidw_error err{};
-    aidw_grid_config c{};
-    if (grid) c = index->config.to_c();
-    detail::raise_if(
-        aidw_knn_stage(queries.xs.data(), queries.ys.data(), n, grid ? &c : nullptr,
-                       grid ? index->cell_start.data() : nullptr,
-                       grid ? index->sorted_point_ids.data() : nullptr,
-                       grid ? index->sorted_x.data() : nullptr,
-                       grid ? index->sorted_y.data() : nullptr, grid ? nullptr : data.xs.data(),
-                       grid ? nullptr : data.ys.data(), m, k,
-                       grid ? AIDW_ENGINE_GRID : AIDW_ENGINE_BRUTE, d2.get(), nullptr, avg.data(),
-                       &k_eff, &exhausted, &err),
-        err);
-    // Materialise n heap vectors (the API's KnnResult shape).  This is host
-    // allocation work, spread over the hardware threads (glibc arenas scale).
-    std::vector<KnnResult> out(n);
+    // The n result vectors (the API's KnnResult shape: host allocation work)
+    // come from the result stash, or are built while the device runs.
+    detail::HostPool& pool = detail::HostPool::instance();
+    detail::ResultStash& stash = detail::ResultStash::instance();
+    std::vector<KnnResult> out;
+    std::thread alloc([&] { out = stash.take(n, k_alloc); });
+    struct Join {
+        std::thread& t;
+        ~Join() {
+            if (t.joinable()) t.join();
+        }
+    } join{alloc};
+    const aidw_index* mirror = grid ? index->mirror() : nullptr;
+    if (mirror) {
+        detail::raise_if(aidw_knn_stage_mirror(queries.xs.data(), queries.ys.data(), n, mirror, k,
+                                               d2.p, nullptr, avg.data(), &k_eff, &exhausted,
+                                               &err),
+                         err);
+    } else {
+        aidw_grid_config c{};
+        if (grid) c = index->config.to_c();
+        detail::raise_if(
+            aidw_knn_stage(queries.xs.data(), queries.ys.data(), n, grid ? &c : nullptr,
+                           grid ? index->cell_start.data() : nullptr,
+                           grid ? index->sorted_point_ids.data() : nullptr,
+                           grid ? index->sorted_x.data() : nullptr,
+                           grid ? index->sorted_y.data() : nullptr, grid ? nullptr : data.xs.data(),
+                           grid ? nullptr : data.ys.data(), m, k,
+                           grid ? AIDW_ENGINE_GRID : AIDW_ENGINE_BRUTE, d2.p, nullptr,
+                           avg.data(), &k_eff, &exhausted, &err),
+            err);
+    }
+    alloc.join();
     const auto ke = static_cast<std::size_t>(std::max(k_eff, 0));
-    parallel([&](std::size_t lo, std::size_t hi) {
+    const double* src = d2.p;
+    pool.parallel_for(n, 4096, [&](std::size_t lo, std::size_t hi) {
         for (std::size_t i = lo; i < hi; ++i) {
-            out[i].distances_sq.assign(d2.get() + i * ke, d2.get() + (i + 1) * ke);
+            out[i].distances_sq.assign(src + i * ke, src + (i + 1) * ke);
             out[i].average_distance = avg[i];
             out[i].exhausted = exhausted != 0;
         }
     });
+    stash.refill(n, k_alloc);
     return out;
 }
 

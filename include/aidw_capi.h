@@ -142,6 +142,29 @@ int aidw_build_index(const double* xs, const double* ys, size_t m, const aidw_gr
                      uint32_t* sorted_ids, uint32_t* cell_start, double* sorted_x,
                      double* sorted_y, aidw_error* err);
 
+/* Device mirror of a GridIndex ("an extra opaque device-mirror
+ * handle member in GridIndex lets the GPU cache uploads").  Same outputs as
+ * aidw_build_index; in addition *mirror receives a handle that keeps the
+ * index's CSR arrays resident in HBM (cell_start, sorted_ids, interleaved
+ * sorted coordinates) on the calling thread's device, so knn_stage calls on
+ * this index upload only their queries.  Release with aidw_index_release
+ * (NULL is a no-op).  The handle is immutable and may be shared by threads. */
+typedef struct aidw_index aidw_index;
+int aidw_build_index_mirror(const double* xs, const double* ys, size_t m,
+                            const aidw_grid_config* cfg, uint32_t* sorted_ids,
+                            uint32_t* cell_start, double* sorted_x, double* sorted_y,
+                            aidw_index** mirror, aidw_error* err);
+void aidw_index_release(aidw_index* mirror);
+/* the mirror's grid (cfg) and point count, for validation by the caller */
+int aidw_index_info(const aidw_index* mirror, aidw_grid_config* cfg, size_t* m);
+
+/* Page-locked host staging from a process-wide cache (cudaHostAlloc'ed
+ * blocks are recycled: pinning is slow, copies from / to pinned memory run
+ * at full PCIe / C2C speed).  NULL if no device / allocation failed (the
+ * caller then uses pageable memory).  Free with aidw_pinned_free. */
+void* aidw_pinned_alloc(size_t bytes);
+void aidw_pinned_free(void* p);
+
 /* ------------------------------------------------------------ kNN (K2) */
 /* knn_stage — knn.hpp:255-271.  Grid engine: pass the GridIndex arrays from
  * build_index (cfg, cell_start, sorted_ids, sorted_x, sorted_y); brute
@@ -157,6 +180,12 @@ int aidw_knn_stage(const double* qx, const double* qy, size_t n, const aidw_grid
                    const double* dy, size_t m, int32_t k, int32_t engine, double* d2_out,
                    uint32_t* idx_out, double* avg_out, int32_t* k_eff_out,
                    int32_t* exhausted_out, aidw_error* err);
+
+/* knn_stage, grid engine, on a device-mirrored index (aidw_build_index_mirror):
+ * identical outputs to aidw_knn_stage with that index's arrays. */
+int aidw_knn_stage_mirror(const double* qx, const double* qy, size_t n, const aidw_index* mirror,
+                          int32_t k, double* d2_out, uint32_t* idx_out, double* avg_out,
+                          int32_t* k_eff_out, int32_t* exhausted_out, aidw_error* err);
 
 /* ------------------------------------------------------------ weighting (K3+K4) */
 /* aidw_predict_all — interpolate.hpp:453-489.  Per query i the caller's

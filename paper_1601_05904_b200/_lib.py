@@ -98,6 +98,14 @@ SIGNATURES = {
     "aidw_nccl_version": (C.c_int32, []),
     "aidw_build_index": (C.c_int, [_dp, _dp, C.c_size_t, C.POINTER(GridConfig), _u32p, _u32p,
                                    _dp, _dp, _ep]),
+    "aidw_build_index_mirror": (C.c_int, [_dp, _dp, C.c_size_t, C.POINTER(GridConfig), _u32p,
+                                          _u32p, _dp, _dp, C.POINTER(C.c_void_p), _ep]),
+    "aidw_index_release": (None, [C.c_void_p]),
+    "aidw_index_info": (C.c_int, [C.c_void_p, C.POINTER(GridConfig), C.POINTER(C.c_size_t)]),
+    "aidw_pinned_alloc": (C.c_void_p, [C.c_size_t]),
+    "aidw_pinned_free": (None, [C.c_void_p]),
+    "aidw_knn_stage_mirror": (C.c_int, [_dp, _dp, C.c_size_t, C.c_void_p, C.c_int32, _dp, _u32p,
+                                        _dp, _i32p, _i32p, _ep]),
     "aidw_knn_stage": (C.c_int, [_dp, _dp, C.c_size_t, C.POINTER(GridConfig), _u32p, _u32p,
                                  _dp, _dp, _dp, _dp, C.c_size_t, C.c_int32, C.c_int32, _dp,
                                  _u32p, _dp, _i32p, _i32p, _ep]),
@@ -160,5 +168,5 @@ def header_symbols(path=HEADER_PATH):
     """Function names declared in include/aidw_capi.h."""
     import re
     text = open(path).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|void)\s+(aidw_\w+)\s*\(", text,
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|void)\s*\*?\s*(aidw_\w+)\s*\(", text,
                                  flags=re.M)))

@@ -111,14 +111,46 @@ class AidwParams:
 GridConfig = L.GridConfig
 
 
+class _Mirror:
+    """Owner of an aidw_index device mirror (released when collected)."""
+    def __init__(self, handle, print_):
+        self.handle, self.print = handle, print_
+
+    def __del__(self):
+        if self.handle:
+            lib().aidw_index_release(self.handle)
+            self.handle = None
+
+
+def _fingerprint(cfg, arrays):
+    """Sizes, grid and 64 sampled entries per array (cf. GridIndex::fingerprint)."""
+    parts = [cfg.cell_width, cfg.n_col, cfg.n_row, cfg.min_x, cfg.min_y]
+    for a in arrays:
+        step = max(1, a.size // 64)
+        parts.append(a.size)
+        parts.append(a[::step].tobytes() + (a[-1:].tobytes() if a.size else b""))
+    return hash(tuple(parts))
+
+
 @dataclass
 class GridIndex:
-    """grid.hpp:131-171 (CSR cell layout)."""
+    """grid.hpp:131-171 (CSR cell layout), plus the device mirror build_index
+    leaves in HBM (knn_stage reuses it while the arrays are unchanged)."""
     config: L.GridConfig
     sorted_point_ids: np.ndarray
     cell_start: np.ndarray
     sorted_x: np.ndarray
     sorted_y: np.ndarray
+    device_mirror: _Mirror | None = None
+
+    def mirror(self):
+        m = self.device_mirror
+        if m is None or m.print != _fingerprint(self.config, self._arrays()):
+            return None
+        return m.handle
+
+    def _arrays(self):
+        return (self.sorted_point_ids, self.cell_start, self.sorted_x, self.sorted_y)
 
     def point_count(self):
         return int(self.sorted_point_ids.size)
@@ -318,9 +350,14 @@ def build_index(data: PointSet, config: L.GridConfig) -> GridIndex:
     cs = np.empty(cells + 1 if m else 1, np.uint32)
     sx, sy = np.empty(m), np.empty(m)
     err = L.Error()
-    _raise(lib().aidw_build_index(_p(data.xs), _p(data.ys), m, C.byref(config), _p(ids, L._u32p),
-                                  _p(cs, L._u32p), _p(sx), _p(sy), C.byref(err)), err)
-    return GridIndex(config, ids, cs, sx, sy)
+    handle = C.c_void_p()
+    _raise(lib().aidw_build_index_mirror(_p(data.xs), _p(data.ys), m, C.byref(config),
+                                         _p(ids, L._u32p), _p(cs, L._u32p), _p(sx), _p(sy),
+                                         C.byref(handle), C.byref(err)), err)
+    g = GridIndex(config, ids, cs, sx, sy)
+    if handle.value:
+        g.device_mirror = _Mirror(handle.value, _fingerprint(config, g._arrays()))
+    return g
 
 
 def knn_stage(queries: PointSet, index: GridIndex | None, data: PointSet, k: int,
@@ -339,6 +376,12 @@ def knn_stage(queries: PointSet, index: GridIndex | None, data: PointSet, k: int
     avg = np.empty(n)
     ke, ex = C.c_int32(), C.c_int32()
     err = L.Error()
+    mirror = index.mirror() if grid else None
+    if mirror:  # the index's arrays are resident in HBM: upload only the queries
+        _raise(lib().aidw_knn_stage_mirror(_p(queries.xs), _p(queries.ys), n, mirror, int(k),
+                                           _p(d2), _p(idx, L._u32p), _p(avg), C.byref(ke),
+                                           C.byref(ex), C.byref(err)), err)
+        return KnnStageResult(d2, idx, avg, bool(ex.value), int(ke.value))
     if grid:
         cfg = index.config
         args = (C.byref(cfg), _p(index.cell_start, L._u32p), _p(index.sorted_point_ids, L._u32p),

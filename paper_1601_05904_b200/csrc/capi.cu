@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <condition_variable>
 #include <functional>
 #include <memory>
@@ -38,6 +39,7 @@
 namespace aidwb {
 
 std::atomic<long long> g_launches{0};
+thread_local long long* t_launch_sink = nullptr;
 thread_local Arena* t_arena = nullptr;
 
 namespace {
@@ -135,6 +137,10 @@ std::string locate_msg(double x, double y) {  // grid.hpp:100-101
 
 // ------------------------------------------------------------ device context
 std::once_flag g_pool_once[64];
+size_t g_pool_keep[64];  // the pool's release threshold per device
+std::once_flag g_pinned_once;
+void* pinned_alloc(size_t bytes);
+void pinned_free(void* p);
 
 int current_device() {
     int count = 0;
@@ -147,13 +153,15 @@ int current_device() {
     std::call_once(g_pool_once[dev & 63], [dev] {
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = std::numeric_limits<uint64_t>::max();
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-            // Reserve a working set once (freed memory stays in the pool), so
-            // later calls never pay pool growth inside a timed stage.
+            // Reserve a working set once (up to 8 GiB of freed memory stays
+            // in the pool), so later calls never pay pool growth inside a
+            // timed stage; memory freed beyond it goes back at sync points.
             size_t free_b = 0, total_b = 0;
             if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
                 const size_t want = std::min<size_t>(free_b / 8, size_t(8) << 30);
+                uint64_t thr = want;
+                g_pool_keep[dev & 63] = want;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
                 void* p = nullptr;
                 if (want && cudaMallocAsync(&p, want, 0) == cudaSuccess) {
                     cudaFreeAsync(p, 0);
@@ -162,6 +170,9 @@ int current_device() {
             }
         }
     });
+    // one 64 MiB page-locked staging block for the drop-in's result copies,
+    // pinned once per process at first device use
+    std::call_once(g_pinned_once, [] { pinned_free(pinned_alloc(1)); });
     return dev;
 }
 
@@ -232,26 +243,34 @@ Extents extents(const double* ax, const double* ay, size_t na, const double* bx,
     return Extents{Box{h[0], h[1], h[2], h[3]}, h[4], h[5]};
 }
 
+// Slots 0-2: failure indices (LLONG_MAX = none); 3-5: counters (0).
 __global__ void fail_init_kernel(long long* __restrict__ d) {
-    if (threadIdx.x < 4) d[threadIdx.x] = LLONG_MAX;
+    if (threadIdx.x < 8) d[threadIdx.x] = threadIdx.x < 3 ? LLONG_MAX : 0;
 }
 
-// Failure indices written by kernels (atomicMin), resolved after sync.
-// Initialised on the stream by a one-warp kernel (no host round trip).
+// Failure indices written by kernels (atomicMin), resolved after sync, and
+// the pass's device counters (recipe queries, kNN candidates) in the same
+// 64-byte block, so one copy returns everything.  Initialised on the stream
+// by a one-warp kernel (no host round trip).
 struct FailFlags {
     DBuf<long long> d;
-    long long h[4];
-    explicit FailFlags(cudaStream_t s) : d(4, s) {
-        for (long long& v : h) v = LLONG_MAX;
-        LAUNCH(fail_init_kernel, 1, 32, 0, s, d.get());
+    long long h[8];
+    explicit FailFlags(cudaStream_t s, bool defer_init = false) : d(8, s) {
+        for (int i = 0; i < 8; ++i) h[i] = i < 3 ? LLONG_MAX : 0;
+        if (!defer_init) init(s);
     }
+    void init(cudaStream_t s) { LAUNCH(fail_init_kernel, 1, 32, 0, s, d.get()); }
     long long* slot(int i) { return d.get() + i; }
+    unsigned long long* counter(int i) { return reinterpret_cast<unsigned long long*>(d.get() + i); }
     void fetch(cudaStream_t s) {
-        d2h(h, d.get(), 4, s);
+        d2h(h, d.get(), 8, s);
         CK(cudaStreamSynchronize(s));
     }
 };
-enum { kFailData = 0, kFailQuery = 1, kFailAlpha = 2 };
+enum { kFailData = 0, kFailQuery = 1, kFailAlpha = 2, kCountAlpha4 = 3, kCountCand = 4,
+       kCountRefCand = 5 };
+
+void record(cudaEvent_t e, cudaStream_t s) { record_event(e, s); }
 
 // Device-side nearest / snap search for the weighting stage when no kNN
 // stage ran (idw mode and the aidw_predict_all drop-in).  Uses a k = 1 grid
@@ -403,65 +422,117 @@ struct PipelineIO {
     double *pred, *alpha;                  // device
 };
 
-// The fused run_pipeline (cli.hpp:217-268) over device-resident buffers.
-void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_stats* st,
-                   Events& ev, cudaStream_t s, std::vector<cudaEvent_t>& marks,
-                   cudaEvent_t& k4b, cudaEvent_t& k4e, cudaEvent_t& knnb, cudaEvent_t& knne,
-                   unsigned long long*& d_a4, DBuf<unsigned long long>& a4buf,
-                   DBuf<unsigned long long>& candbuf) {
+// Timing events of one fused pass (stage marks, kNN kernel, K4 launches).
+struct PassEvents {
+    cudaEvent_t build0 = nullptr, build1 = nullptr, knn1 = nullptr, interp1 = nullptr;
+    cudaEvent_t knnb = nullptr, knne = nullptr, k4b = nullptr, k4e = nullptr;
+    void create() {
+        for (cudaEvent_t* e : {&build0, &build1, &knn1, &interp1, &knnb, &knne, &k4b, &k4e})
+            CK(cudaEventCreate(e));
+    }
+    void destroy() {
+        for (cudaEvent_t* e : {&build0, &build1, &knn1, &interp1, &knnb, &knne, &k4b, &k4e}) {
+            if (*e) cudaEventDestroy(*e);
+            *e = nullptr;
+        }
+    }
+};
+
+// Every host-side scalar of a fused pass (the reference's set-up
+// expressions), computed before any device work is enqueued: the kernels
+// receive only these, so a pass with the same plan and buffers is the same
+// sequence of launches (what the CUDA-graph cache relies on).
+struct PassPlan {
+    bool idw = false;
+    Extents ext{};
+    aidw_params params{};  // k clamped to m
+    WeightMode wmode = WeightMode::fp32;
+    aidw_grid_config gc{};  // the kNN grid (grid engine)
+    double r_exp = 0.0;
+    WeightFrame frame{};
+    bool own_g4 = false;  // K4 record order from a separate factor-4 grid
+    aidw_grid_config g4c{};
+};
+
+// Validation + extents (the one host round trip before the pass) + set-up
+// (cli.hpp:217-268, with the reference's exception order).
+PassPlan plan_pass(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_stats* st,
+                   cudaStream_t s) {
     if (cfg.workers < 0)
         throw Failure(AIDW_ERR_INVALID_ARGUMENT, "resolve_workers: worker count must be >= 0");
     const size_t m = io.m, n = io.n;
     if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set is empty");
     if (!io.dz) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set carries no values");
-    FailFlags fails(s);
-    a4buf.alloc(1, s);
-    candbuf.alloc(2, s);
-    CK(cudaMemsetAsync(a4buf.get(), 0, sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(candbuf.get(), 0, 2 * sizeof(unsigned long long), s));
-    d_a4 = a4buf.get();
-    const WeightMode wmode = weight_mode(cfg.variant, 0);
-    WeightTimes wt;
-    wt.k4_begin = k4b = ev.make();
-    wt.k4_end = k4e = ev.make();
-    wt.d_alpha4 = d_a4;
-
+    PassPlan pl;
+    pl.wmode = weight_mode(cfg.variant, 0);
     // bbox(data ∪ queries) and the value hull
-    Extents ext;
     if (cfg.use_bbox) {
-        ext = extents(nullptr, nullptr, 0, nullptr, nullptr, 0, io.dz, m, s);
-        ext.box = Box{cfg.bbox[0], cfg.bbox[1], cfg.bbox[2], cfg.bbox[3]};
+        pl.ext = extents(nullptr, nullptr, 0, nullptr, nullptr, 0, io.dz, m, s);
+        pl.ext.box = Box{cfg.bbox[0], cfg.bbox[1], cfg.bbox[2], cfg.bbox[3]};
     } else {
-        ext = extents(io.dx, io.dy, m, io.qx, io.qy, n, io.dz, m, s);
+        pl.ext = extents(io.dx, io.dy, m, io.qx, io.qy, n, io.dz, m, s);
     }
-    const cudaEvent_t e_build0 = ev.make(), e_build1 = ev.make(), e_knn1 = ev.make(),
-                      e_interp1 = ev.make();
-    marks = {e_build0, e_build1, e_knn1, e_interp1};
-
+    pl.frame = make_frame(pl.ext.box, pl.ext.zlo, pl.ext.zhi);
     if (cfg.mode == AIDW_MODE_IDW) {
         if (!(cfg.alpha > 0.0) || !std::isfinite(cfg.alpha))
             throw Failure(AIDW_ERR_INVALID_ARGUMENT, "idw_predict_all: alpha must be positive finite");
-        CK(cudaEventRecord(e_build0, s));
-        CK(cudaEventRecord(e_build1, s));
-        CK(cudaEventRecord(e_knn1, s));
-        DBuf<double> alpha_q(n, s);
-        if (n) LAUNCH(fill_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, alpha_q.get(), n, cfg.alpha);
-        weighting_stage(io.dx, io.dy, io.dz, m, io.qx, io.qy, n, alpha_q.get(), ext, wmode,
-                        io.pred, io.alpha, fails, &wt, s);
-        CK(cudaEventRecord(e_interp1, s));
-        fails.fetch(s);
+        pl.idw = true;
         if (st) st->k_effective = 0;
-        return;
+        return pl;
     }
-
     // k clamp (cli.hpp:237-238): the reference converts k to size_t first,
     // so a negative k clamps to m as well.
-    aidw_params params = cfg.params;
-    params.k = static_cast<int32_t>(
+    pl.params = cfg.params;
+    pl.params.k = static_cast<int32_t>(
         std::min<size_t>(static_cast<size_t>(static_cast<int64_t>(cfg.params.k)), m));
-    if (st) st->k_effective = params.k;
-    const int k = params.k;
+    if (st) st->k_effective = pl.params.k;
+    const double area = pl.params.area > 0.0 ? pl.params.area : pl.ext.box.area();
+    // the reference's order (cli.hpp:240-259): the grid engine's cell width
+    // rejects a zero-area bbox (invalid_argument) before any query runs; the
+    // per-query area failure of aidw_predict_all needs a query to fail on
+    if (cfg.engine == AIDW_ENGINE_GRID)
+        pl.gc = make_grid_config_h(pl.ext.box, choose_cell_width_h(m, pl.ext.box, cfg.cell_factor));
+    validate_params(pl.params);  // aidw_predict_all's params.validate() (interpolate.hpp:457)
+    if (n > 0 && (!(area > 0.0) || !std::isfinite(area)))
+        throw Failure(AIDW_ERR_RUNTIME,
+                      "aidw_predict_all: query 0: expected_nn_distance: area must be positive finite", 0);
+    pl.r_exp = 1.0 / (2.0 * std::sqrt(static_cast<double>(m) / area));  // adaptive.hpp:27
+    // K4 record order: cell order of the factor-4 grid over the bbox — the
+    // kNN grid when it is one, else built for K4 — so the FP32 sums depend on
+    // the inputs only, never on the kNN engine or cell factor
+    if (pl.wmode == WeightMode::fp32 && m > 4096 &&  // same rule as nearest_search
+        !(cfg.engine == AIDW_ENGINE_GRID && cfg.cell_factor == 4.0)) {
+        try {
+            pl.g4c = make_grid_config_h(pl.ext.box, choose_cell_width_h(m, pl.ext.box, 4.0));
+            pl.own_g4 = true;
+        } catch (const Failure&) {
+            pl.own_g4 = false;
+        }
+    }
+    return pl;
+}
 
+// The device work of one fused pass (cli.hpp:217-268): no host round trip,
+// no allocation outside the call's workspace (when it fits).
+void enqueue_pass(const PassPlan& pl, const PipelineIO& io, const aidw_run_config& cfg,
+                  const PassEvents& pe, FailFlags& fails, cudaStream_t s) {
+    const size_t m = io.m, n = io.n;
+    WeightTimes wt;
+    wt.k4_begin = pe.k4b;
+    wt.k4_end = pe.k4e;
+    wt.d_alpha4 = fails.counter(kCountAlpha4);
+    if (pl.idw) {
+        record(pe.build0, s);
+        record(pe.build1, s);
+        record(pe.knn1, s);
+        DBuf<double> alpha_q(n, s);
+        if (n) LAUNCH(fill_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, alpha_q.get(), n, cfg.alpha);
+        weighting_stage(io.dx, io.dy, io.dz, m, io.qx, io.qy, n, alpha_q.get(), pl.ext, pl.wmode,
+                        io.pred, io.alpha, fails, &wt, s);
+        record(pe.interp1, s);
+        return;
+    }
+    const int k = pl.params.k;
     KnnArgs a;
     a.qx = io.qx;
     a.qy = io.qy;
@@ -469,42 +540,24 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     a.m = m;
     a.k = k;
     a.k_eff = k;
-    a.candidates = candbuf.get();
-    a.ref_candidates = candbuf.get() + 1;
-    const double area = params.area > 0.0 ? params.area : ext.box.area();
-    const double r_exp_arg = static_cast<double>(m) / area;
-    // the reference's order (cli.hpp:240-259): the grid engine's cell width
-    // rejects a zero-area bbox (invalid_argument) before any query runs; the
-    // per-query area failure of aidw_predict_all needs a query to fail on
-    aidw_grid_config gc{};
-    if (cfg.engine == AIDW_ENGINE_GRID)
-        gc = make_grid_config_h(ext.box, choose_cell_width_h(m, ext.box, cfg.cell_factor));
-    if (n > 0 && (!(area > 0.0) || !std::isfinite(area)))
-        throw Failure(AIDW_ERR_RUNTIME,
-                      "aidw_predict_all: query 0: expected_nn_distance: area must be positive finite", 0);
-    const double r_exp = 1.0 / (2.0 * std::sqrt(r_exp_arg));  // adaptive.hpp:27
-    const WeightFrame frame = make_frame(ext.box, ext.zlo, ext.zhi);
-    a.snap_sq = frame.snap_sq;
+    a.candidates = fails.counter(kCountCand);
+    a.ref_candidates = fails.counter(kCountRefCand);
+    a.snap_sq = pl.frame.snap_sq;
     a.compute_alpha = 1;
-    a.ap = alpha_params_h(params, r_exp);
+    a.ap = alpha_params_h(pl.params, pl.r_exp);
     a.fail_alpha = fails.slot(kFailAlpha);
-
     DBuf<double> alpha_s(n, s), d2min_s(n, s);
     DBuf<uint32_t> nn_s(n, s), snap_s(n, s), perm, qcell;
     a.alpha_s = alpha_s.get();
     a.d2min_s = d2min_s.get();
     a.nn_s = nn_s.get();
     a.snap_s = snap_s.get();
-    knnb = ev.make();
-    knne = ev.make();
-
     DeviceGrid g;  // lives until the weighting stage has read its cell order
     if (cfg.engine == AIDW_ENGINE_GRID) {
-        validate_params(params);
-        CK(cudaEventRecord(e_build0, s));
-        build_grid_device(io.dx, io.dy, m, gc, g, fails.slot(kFailData), s);
-        CK(cudaEventRecord(e_build1, s));
-        const GridGeom geom = make_geom(gc);
+        record(pe.build0, s);
+        build_grid_device(io.dx, io.dy, m, pl.gc, g, fails.slot(kFailData), s);
+        record(pe.build1, s);
+        const GridGeom geom = make_geom(pl.gc);
         sort_queries_by_cell(io.qx, io.qy, n, geom, perm, qcell, fails.slot(kFailQuery), s);
         a.g = geom;
         a.cell_start = g.cell_start.get();
@@ -512,39 +565,28 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
         a.sorted_xy = g.sorted_xy.get();
         a.perm = perm.get();
         a.qcell = qcell.get();
-        CK(cudaEventRecord(knnb, s));
+        record(pe.knnb, s);
         run_knn_grid(a, s);
-        CK(cudaEventRecord(knne, s));
-        CK(cudaEventRecord(e_knn1, s));
+        record(pe.knne, s);
+        record(pe.knn1, s);
     } else {
-        validate_params(params);
-        CK(cudaEventRecord(e_build0, s));
-        CK(cudaEventRecord(e_build1, s));
+        record(pe.build0, s);
+        record(pe.build1, s);
         a.dx = io.dx;
         a.dy = io.dy;
-        CK(cudaEventRecord(knnb, s));
+        record(pe.knnb, s);
         run_knn_brute(a, s);
-        CK(cudaEventRecord(knne, s));
-        CK(cudaEventRecord(e_knn1, s));
+        record(pe.knne, s);
+        record(pe.knn1, s);
     }
-
     WeightData wd{io.dx, io.dy, io.dz, m};
-    // K4 record order: cell order of the factor-4 grid over the bbox — the
-    // kNN grid when it is one, else built here — so the FP32 sums depend on
-    // the inputs only, never on the kNN engine or cell factor
     DeviceGrid g4;
-    if (wmode == WeightMode::fp32 && m > 4096) {  // same rule as nearest_search
-        if (cfg.engine == AIDW_ENGINE_GRID && cfg.cell_factor == 4.0) {
+    if (pl.wmode == WeightMode::fp32 && m > 4096) {
+        if (pl.own_g4) {
+            build_grid_device(io.dx, io.dy, m, pl.g4c, g4, fails.slot(kFailData), s);
+            set_order(wd, g4);
+        } else if (cfg.engine == AIDW_ENGINE_GRID && cfg.cell_factor == 4.0) {
             set_order(wd, g);
-        } else {
-            try {
-                const aidw_grid_config c4 =
-                    make_grid_config_h(ext.box, choose_cell_width_h(m, ext.box, 4.0));
-                build_grid_device(io.dx, io.dy, m, c4, g4, fails.slot(kFailData), s);
-                set_order(wd, g4);
-            } catch (const Failure&) {
-                wd.order = nullptr;
-            }
         }
     }
     WeightQueries q;
@@ -556,12 +598,16 @@ void pipeline_core(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     q.d2min_s = d2min_s.get();
     q.nn_s = nn_s.get();
     q.snap_s = snap_s.get();
-    if (wmode != WeightMode::fp32)
-        weighting_fp64(q, wd, frame, wmode == WeightMode::fp64_blocked, io.pred, io.alpha, &wt, s);
+    if (pl.wmode != WeightMode::fp32)
+        weighting_fp64(q, wd, pl.frame, pl.wmode == WeightMode::fp64_blocked, io.pred, io.alpha, &wt, s);
     else
-        weighting_fp32(q, wd, frame, io.pred, io.alpha, &wt, s);
-    CK(cudaEventRecord(e_interp1, s));
-    fails.fetch(s);
+        weighting_fp32(q, wd, pl.frame, io.pred, io.alpha, &wt, s);
+    record(pe.interp1, s);
+}
+
+// The reference's exceptions for the failures the pass recorded (smallest
+// failing index; knn_stage's query error first, as the stages run).
+void raise_pass_failures(const FailFlags& fails) {
     if (fails.h[kFailQuery] != LLONG_MAX)
         throw Failure(AIDW_ERR_RUNTIME,
                       "knn_stage: query " + std::to_string(fails.h[kFailQuery]) +
@@ -636,6 +682,19 @@ struct ArenaScope {
         // normally a no-op (the call synchronised); on an exception path it
         // keeps in-flight kernels off a recycled workspace
         if (cudaStreamSynchronize(a.stream) != cudaSuccess) cudaGetLastError();
+        // much larger than the last few calls needed (> 256 MiB, 8x their
+        // use, 3 calls in a row): give it back, the next call re-sizes it
+        a.small = (a.cap > (size_t(256) << 20) && (a.used + a.overflow) * 8 < a.cap) ? a.small + 1 : 0;
+        if (a.small >= 3 && !a.overflow) {
+            cudaFreeAsync(a.base, a.stream);
+            if (cudaStreamSynchronize(a.stream) != cudaSuccess) cudaGetLastError();
+            a.base = nullptr;
+            a.cap = 0;
+            a.small = 0;
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+                cudaMemPoolTrimTo(pool, g_pool_keep[dev & 63]);
+        }
         if (a.overflow) {  // grow for the next call, from the warm pool
             if (a.base) cudaFreeAsync(a.base, a.stream);
             a.base = nullptr;
@@ -656,18 +715,172 @@ struct ArenaScope {
     ArenaScope& operator=(const ArenaScope&) = delete;
 };
 
+// ---- CUDA-graph cache of fused passes.  A pass whose plan, buffers and
+// workspace are those of an earlier pass is the same launch sequence, so it
+// is captured once (on its second occurrence: the first run sized the
+// workspace) and replayed with one cudaGraphLaunch — ~40 kernel launches of
+// host overhead become one, which is most of a 10K x 10K pass.  The key
+// holds every host value a kernel of the pass receives: the plan (bbox, value
+// hull, grid, k, alpha parameters), the run config, the device buffers, the
+// workspace base / offset, the device and the process-wide weighting knobs.
+struct GraphKeyPod {
+    int dev, precision, recipe;
+    size_t m, n, slab, arena_cap, arena_used;
+    const void* ptr[8];
+    aidw_run_config cfg;
+    double ext[6];
+};
+
+struct GraphEntry {
+    std::vector<unsigned char> key;
+    cudaGraphExec_t exec = nullptr;
+    PassEvents ev;
+    size_t used_after = 0;  // workspace offset after the captured pass
+    long long kernels = 0;  // kernel nodes (counted as launches on replay)
+    long long uses = 0;
+};
+
+std::mutex g_graph_mu;
+std::vector<std::unique_ptr<GraphEntry>> g_graphs;      // most recent last, <= kMaxGraphs
+std::vector<std::vector<unsigned char>> g_graph_seen;    // keys run once without overflow
+constexpr size_t kMaxGraphs = 16;
+std::atomic<int> g_graphs_enabled{[] {
+    const char* e = std::getenv("AIDW_GRAPHS");
+    return (e && e[0] == '0') ? 0 : 1;
+}()};
+std::atomic<long long> g_graph_replays{0}, g_graph_captures{0};
+
+std::vector<unsigned char> graph_key(const PipelineIO& io, const aidw_run_config& cfg,
+                                     const PassPlan& pl, const Arena* arena, cudaStream_t s) {
+    GraphKeyPod k;
+    std::memset(&k, 0, sizeof k);
+    CK(cudaGetDevice(&k.dev));
+    k.precision = g_precision.load();
+    k.recipe = alpha4_recipe_enabled() ? 1 : 0;
+    k.m = io.m;
+    k.n = io.n;
+    k.slab = query_slab(weight_split(io.m).chunks);
+    k.arena_cap = arena->cap;
+    k.arena_used = arena->used;
+    const void* p[8] = {io.dx, io.dy, io.dz, io.qx, io.qy, io.pred, io.alpha, arena->base};
+    std::memcpy(k.ptr, p, sizeof p);
+    k.cfg = cfg;
+    const double e[6] = {pl.ext.box.min_x, pl.ext.box.min_y, pl.ext.box.max_x, pl.ext.box.max_y,
+                         pl.ext.zlo, pl.ext.zhi};
+    std::memcpy(k.ext, e, sizeof e);
+    (void)s;
+    std::vector<unsigned char> out(sizeof k);
+    std::memcpy(out.data(), &k, sizeof k);
+    return out;
+}
+
+// Runs the pass's device work: a cached graph, a fresh capture, or eagerly.
+// Returns the events that time it.
+const PassEvents& run_pass(const PassPlan& pl, const PipelineIO& io, const aidw_run_config& cfg,
+                           FailFlags& fails, PassEvents& eager_ev, Arena* arena, cudaStream_t s) {
+    const bool graphable = g_graphs_enabled.load() && arena && arena->stream == s && arena->base;
+    std::vector<unsigned char> key;
+    if (graphable) {
+        key = graph_key(io, cfg, pl, arena, s);
+        std::unique_lock<std::mutex> lk(g_graph_mu);
+        for (size_t i = 0; i < g_graphs.size(); ++i) {
+            if (g_graphs[i]->key == key) {
+                GraphEntry* e = g_graphs[i].get();
+                std::rotate(g_graphs.begin() + i, g_graphs.begin() + i + 1, g_graphs.end());
+                lk.unlock();
+                // the workspace holds the same buffers at the same offsets:
+                // advance it as the captured pass did
+                arena->used = e->used_after;
+                CK(cudaGraphLaunch(e->exec, s));
+                g_launches.fetch_add(e->kernels, std::memory_order_relaxed);
+                ++e->uses;
+                g_graph_replays.fetch_add(1);
+                return e->ev;
+            }
+        }
+        const bool seen = std::find(g_graph_seen.begin(), g_graph_seen.end(), key) != g_graph_seen.end();
+        lk.unlock();
+        if (seen) {  // second occurrence: capture, keep, replay
+            auto e = std::make_unique<GraphEntry>();
+            e->key = key;
+            e->ev.create();
+            const size_t used0 = arena->used, over0 = arena->overflow;
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            bool ok = true;
+            t_launch_sink = &e->kernels;
+            try {
+                fails.init(s);
+                enqueue_pass(pl, io, cfg, e->ev, fails, s);
+            } catch (...) {
+                ok = false;
+            }
+            t_launch_sink = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+            ok = ok && ce == cudaSuccess && arena->overflow == over0;
+            if (ok && cudaGraphInstantiate(&e->exec, graph, 0) != cudaSuccess) ok = false;
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            if (ok) {
+                e->used_after = arena->used;
+                CK(cudaGraphLaunch(e->exec, s));
+                g_launches.fetch_add(e->kernels);
+                g_graph_captures.fetch_add(1);
+                const PassEvents* ev = &e->ev;
+                std::lock_guard<std::mutex> g(g_graph_mu);
+                g_graphs.push_back(std::move(e));
+                if (g_graphs.size() > kMaxGraphs) {
+                    GraphEntry* old = g_graphs.front().get();
+                    cudaStreamSynchronize(s);
+                    cudaGraphExecDestroy(old->exec);
+                    old->ev.destroy();
+                    g_graphs.erase(g_graphs.begin());
+                }
+                return *ev;
+            }
+            // capture failed (e.g. the workspace overflowed inside it): run eagerly
+            if (e->exec) cudaGraphExecDestroy(e->exec);
+            e->ev.destroy();
+            arena->used = used0;
+            arena->overflow = over0;
+        }
+    }
+    eager_ev.create();
+    fails.init(s);
+    enqueue_pass(pl, io, cfg, eager_ev, fails, s);
+    if (graphable && arena->overflow == 0) {
+        std::lock_guard<std::mutex> g(g_graph_mu);
+        if (std::find(g_graph_seen.begin(), g_graph_seen.end(), key) == g_graph_seen.end()) {
+            g_graph_seen.push_back(key);
+            if (g_graph_seen.size() > 4 * kMaxGraphs) g_graph_seen.erase(g_graph_seen.begin());
+        }
+    }
+    return eager_ev;
+}
+
+// A workspace for the call unless the caller (e.g. aidw_run_pipeline, whose
+// uploads live in it too) already opened one on this stream.
+struct MaybeArena {
+    std::unique_ptr<ArenaScope> own;
+    explicit MaybeArena(cudaStream_t s) {
+        if (!(t_arena && t_arena->stream == s)) own = std::make_unique<ArenaScope>(s);
+    }
+};
+
 void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_stats* st,
                     cudaStream_t s, double h2d_ms, const std::chrono::steady_clock::time_point& t0,
                     double* h_pred, double* h_alpha) {
     const long long launches0 = g_launches.load();
-    ArenaScope arena(s);  // declared first: destroyed after every DBuf of the call
-    Events ev;
-    std::vector<cudaEvent_t> marks;
-    cudaEvent_t k4b = nullptr, k4e = nullptr, knnb = nullptr, knne = nullptr;
-    unsigned long long* d_a4 = nullptr;
-    DBuf<unsigned long long> a4buf, candbuf;
+    MaybeArena arena(s);  // declared first: destroyed after every DBuf of the call
     aidw_run_stats local{};
-    pipeline_core(io, cfg, &local, ev, s, marks, k4b, k4e, knnb, knne, d_a4, a4buf, candbuf);
+    const PassPlan pl = plan_pass(io, cfg, &local, s);
+    FailFlags fails(s, /*defer_init=*/true);
+    PassEvents eager;
+    struct EventsGuard {
+        PassEvents& e;
+        ~EventsGuard() { e.destroy(); }
+    } guard{eager};
+    const PassEvents& ev = run_pass(pl, io, cfg, fails, eager, t_arena, s);
     double d2h_ms = 0.0;
     if (h_pred) {
         const auto c0 = std::chrono::steady_clock::now();
@@ -676,28 +889,24 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
         CK(cudaStreamSynchronize(s));
         d2h_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
     }
-    CK(cudaStreamSynchronize(s));
+    fails.fetch(s);  // failure indices and pass counters, one copy
+    raise_pass_failures(fails);
     if (st) {
         *st = local;
         // idw mode has no build / kNN stage (cli.hpp:227-234): exactly 0 ms
         const bool idw = cfg.mode == AIDW_MODE_IDW;
-        st->build_ms = idw ? 0.0 : Events::ms(marks[0], marks[1]);
-        st->knn_ms = idw ? 0.0 : Events::ms(marks[1], marks[2]);
-        st->interp_ms = Events::ms(marks[2], marks[3]);
-        st->weight_kernel_ms = Events::ms(k4b, k4e);
-        st->knn_kernel_ms = Events::ms(knnb, knne);
+        st->build_ms = idw ? 0.0 : Events::ms(ev.build0, ev.build1);
+        st->knn_ms = idw ? 0.0 : Events::ms(ev.build1, ev.knn1);
+        st->interp_ms = Events::ms(ev.knn1, ev.interp1);
+        st->weight_kernel_ms = Events::ms(ev.k4b, ev.k4e);
+        st->knn_kernel_ms = idw ? 0.0 : Events::ms(ev.knnb, ev.knne);
         st->h2d_ms = h2d_ms;
         st->d2h_ms = d2h_ms;
         st->worker_count = cfg.workers > 0 ? cfg.workers : 1;
         st->pairs = static_cast<int64_t>(io.m) * static_cast<int64_t>(io.n);
-        unsigned long long h = 0;
-        if (a4buf.get()) CK(cudaMemcpy(&h, a4buf.get(), sizeof h, cudaMemcpyDeviceToHost));
-        st->alpha4_queries = static_cast<int64_t>(h);
-        h = 0;
-        unsigned long long hc[2] = {0, 0};
-        if (candbuf.get()) CK(cudaMemcpy(hc, candbuf.get(), sizeof hc, cudaMemcpyDeviceToHost));
-        st->knn_candidates = static_cast<int64_t>(hc[0]);
-        st->knn_ref_candidates = static_cast<int64_t>(hc[1]);
+        st->alpha4_queries = fails.h[kCountAlpha4];
+        st->knn_candidates = fails.h[kCountCand];
+        st->knn_ref_candidates = fails.h[kCountRefCand];
         st->kernel_launches = g_launches.load() - launches0;
         st->total_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1005,10 +1214,178 @@ bool raster_multi(const std::vector<int>& devs, const double* dx, const double* 
     return ok;
 }
 
+// build_index's argument checks (grid.hpp:178-183).
+void build_index_checks(size_t m, const aidw_grid_config* cfg) {
+    if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: data set is empty");
+    if (m > static_cast<size_t>(std::numeric_limits<uint32_t>::max()) - 1)
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: too many points for 32-bit ids");
+    if (!cfg || cfg->n_col < 1 || cfg->n_row < 1 || !(cfg->cell_width > 0.0))
+        throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: invalid grid configuration");
+}
+
+// knn_stage's k_eff / exhausted and per-query preconditions (knn.hpp:255-271,
+// grid_knn :212-223, brute_force_knn :100-108): the errors every query would
+// raise are reported for query 0, the smallest index.
+int knn_stage_prologue(size_t n, size_t m, int32_t k, bool grid, int32_t* k_eff_out,
+                       int32_t* exhausted_out) {
+    const int k_eff = grid ? static_cast<int>(std::min<int64_t>(k, static_cast<int64_t>(m))) : k;
+    const bool exhausted = grid && static_cast<int64_t>(m) < k;
+    if (k_eff_out) *k_eff_out = k_eff;
+    if (exhausted_out) *exhausted_out = exhausted ? 1 : 0;
+    if (n == 0) return k_eff;
+    if (grid) {
+        if (m == 0) throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: grid_knn: index holds no points", 0);
+        if (k < 1) throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: grid_knn: k must be >= 1", 0);
+    } else {
+        if (m == 0)
+            throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: brute_force_knn: data set is empty", 0);
+        if (k < 1 || static_cast<size_t>(k) > m)
+            throw Failure(AIDW_ERR_RUNTIME,
+                          "knn_stage: query 0: brute_force_knn: k = " + std::to_string(k) +
+                              " outside [1, " + std::to_string(m) + "]", 0);
+    }
+    return k_eff;
+}
+
+// The grid engine of knn_stage over device CSR arrays: queries uploaded,
+// sorted by cell (locate failures -> the smallest failing query), K2, and
+// the flat outputs copied back to the caller's buffers.
+void knn_grid_stage(const double* qx, const double* qy, size_t n, const aidw_grid_config& cfg,
+                    const uint32_t* d_cs, const uint32_t* d_ids, const double2* d_xy, size_t m,
+                    int k, int k_eff, double* d2_out, uint32_t* idx_out, double* avg_out,
+                    cudaStream_t s) {
+    FailFlags fails(s);
+    DBuf<double> dqx, dqy, d2(n * static_cast<size_t>(k_eff), s), avg(n, s);
+    DBuf<uint32_t> ids(idx_out ? n * static_cast<size_t>(k_eff) : 0, s), perm, qcell;
+    h2d(dqx, qx, n, s);
+    h2d(dqy, qy, n, s);
+    const GridGeom geom = make_geom(cfg);
+    sort_queries_by_cell(dqx.get(), dqy.get(), n, geom, perm, qcell, fails.slot(kFailQuery), s);
+    KnnArgs a;
+    a.qx = dqx.get();
+    a.qy = dqy.get();
+    a.n = n;
+    a.m = m;
+    a.k = k;
+    a.k_eff = k_eff;
+    a.d2_out = d2.get();
+    a.id_out = idx_out ? ids.get() : nullptr;
+    a.avg_out = avg.get();
+    a.g = geom;
+    a.cell_start = d_cs;
+    a.sorted_ids = d_ids;
+    a.sorted_xy = d_xy;
+    a.perm = perm.get();
+    a.qcell = qcell.get();
+    // a query outside the grid makes K2 skip it (locate fails the same way
+    // in both kernels); the error is raised after the single synchronisation
+    run_knn_grid(a, s);
+    d2h(d2_out, d2.get(), n * static_cast<size_t>(k_eff), s);
+    if (idx_out) d2h(idx_out, ids.get(), n * static_cast<size_t>(k_eff), s);
+    d2h(avg_out, avg.get(), n, s);
+    fails.fetch(s);
+    if (fails.h[kFailQuery] != LLONG_MAX) {
+        const long long i = fails.h[kFailQuery];
+        throw Failure(AIDW_ERR_RUNTIME,
+                      "knn_stage: query " + std::to_string(i) + ": " + locate_msg(qx[i], qy[i]), i);
+    }
+}
+
+// Page-locked staging cache (aidw_pinned_alloc): freed blocks are kept (up
+// to 2 GiB) and reused for requests they cover without wasting over half.
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;
+std::map<void*, size_t> g_pin_size;
+size_t g_pin_cached = 0;
+
+void* pinned_alloc(size_t bytes) {
+    if (bytes == 0) bytes = 1;
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto it = g_pin_free.lower_bound(bytes);  // the smallest cached block that fits
+        if (it != g_pin_free.end()) {
+            void* p = it->second;
+            g_pin_cached -= it->first;
+            g_pin_free.erase(it);
+            return p;
+        }
+    }
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    // at least 64 MiB: pinning costs ~1 ms per 4 MiB, paid once per block
+    const size_t size =
+        std::max<size_t>((bytes + (size_t(1) << 20) - 1) & ~((size_t(1) << 20) - 1), size_t(64) << 20);
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, size, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_size[p] = size;
+    return p;
+}
+
+void pinned_free(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_size.find(p);
+    if (it == g_pin_size.end()) return;
+    const size_t size = it->second;
+    if (g_pin_cached + size > (size_t(2) << 30)) {
+        g_pin_size.erase(it);
+        cudaFreeHost(p);
+        return;
+    }
+    g_pin_free.emplace(size, p);
+    g_pin_cached += size;
+}
+
+// Makes `dev` current for a scope (mirror handles belong to one device).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        CK(cudaGetDevice(&prev));
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 }  // namespace
 }  // namespace aidwb
 
 using namespace aidwb;
+
+// The device mirror behind aidw_index* (include/aidw_capi.h): the grid's CSR
+// arrays resident on device `dev`, allocated and released on its own stream.
+struct aidw_index {
+    int dev = 0;
+    aidw_grid_config cfg{};
+    size_t m = 0;
+    cudaStream_t s = nullptr;
+    DeviceGrid g;
+    ~aidw_index() {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+        g.cell_start.release();  // back to the pool, on s
+        g.sorted_ids.release();
+        g.sorted_x.release();
+        g.sorted_y.release();
+        g.sorted_xy.release();
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+        if (prev >= 0) cudaSetDevice(prev);
+        cudaGetLastError();
+    }
+};
 
 extern "C" {
 
@@ -1043,11 +1420,7 @@ int aidw_build_index(const double* xs, const double* ys, size_t m, const aidw_gr
                      uint32_t* sorted_ids, uint32_t* cell_start, double* sorted_x,
                      double* sorted_y, aidw_error* err) {
     return guarded(err, [&] {
-        if (m == 0) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: data set is empty");
-        if (m > static_cast<size_t>(std::numeric_limits<uint32_t>::max()) - 1)
-            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: too many points for 32-bit ids");
-        if (!cfg || cfg->n_col < 1 || cfg->n_row < 1 || !(cfg->cell_width > 0.0))
-            throw Failure(AIDW_ERR_INVALID_ARGUMENT, "build_index: invalid grid configuration");
+        build_index_checks(m, cfg);
         StreamScope ss;
         cudaStream_t s = ss.s;
         FailFlags fails(s);
@@ -1079,78 +1452,119 @@ int aidw_knn_stage(const double* qx, const double* qy, size_t n, const aidw_grid
         const bool grid = engine == AIDW_ENGINE_GRID;
         if (grid && (!cfg || !cell_start || (m > 0 && (!sorted_ids || !sorted_x || !sorted_y))))
             throw Failure(AIDW_ERR_INVALID_ARGUMENT, "knn_stage: grid engine requires a grid index");
-        int k_eff = grid ? static_cast<int>(std::min<int64_t>(k, static_cast<int64_t>(m))) : k;
-        const bool exhausted = grid && static_cast<int64_t>(m) < k;
-        if (k_eff_out) *k_eff_out = k_eff;
-        if (exhausted_out) *exhausted_out = exhausted ? 1 : 0;
+        const int k_eff = knn_stage_prologue(n, m, k, grid, k_eff_out, exhausted_out);
         if (n == 0) return;
-        if (grid) {
-            if (m == 0) throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: grid_knn: index holds no points", 0);
-            if (k < 1) throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: grid_knn: k must be >= 1", 0);
-        } else {
-            if (m == 0)
-                throw Failure(AIDW_ERR_RUNTIME, "knn_stage: query 0: brute_force_knn: data set is empty", 0);
-            if (k < 1 || static_cast<size_t>(k) > m)
-                throw Failure(AIDW_ERR_RUNTIME,
-                              "knn_stage: query 0: brute_force_knn: k = " + std::to_string(k) +
-                                  " outside [1, " + std::to_string(m) + "]", 0);
-        }
         StreamScope ss;
         cudaStream_t s = ss.s;
-        FailFlags fails(s);
-        DBuf<double> dqx, dqy, d2(n * static_cast<size_t>(k_eff), s), avg(n, s);
-        DBuf<uint32_t> ids(idx_out ? n * static_cast<size_t>(k_eff) : 0, s);
-        h2d(dqx, qx, n, s);
-        h2d(dqy, qy, n, s);
-        KnnArgs a;
-        a.qx = dqx.get();
-        a.qy = dqy.get();
-        a.n = n;
-        a.m = m;
-        a.k = k;
-        a.k_eff = k_eff;
-        a.d2_out = d2.get();
-        a.id_out = idx_out ? ids.get() : nullptr;
-        a.avg_out = avg.get();
-        DBuf<double> ddx, ddy, sx, sy;
-        DBuf<double2> sxy;
-        DBuf<uint32_t> cs, sid, perm, qcell;
         if (grid) {
             const size_t cells = static_cast<size_t>(cfg->n_col) * static_cast<size_t>(cfg->n_row);
+            DBuf<double> sx, sy;
+            DBuf<double2> sxy;
+            DBuf<uint32_t> cs, sid;
             h2d(cs, cell_start, cells + 1, s);
             h2d(sid, sorted_ids, m, s);
             h2d(sx, sorted_x, m, s);
             h2d(sy, sorted_y, m, s);
-            const GridGeom geom = make_geom(*cfg);
-            sort_queries_by_cell(dqx.get(), dqy.get(), n, geom, perm, qcell, fails.slot(kFailQuery), s);
-            fails.fetch(s);
-            if (fails.h[kFailQuery] != LLONG_MAX) {
-                const long long i = fails.h[kFailQuery];
-                throw Failure(AIDW_ERR_RUNTIME,
-                              "knn_stage: query " + std::to_string(i) + ": " + locate_msg(qx[i], qy[i]), i);
-            }
-            a.g = geom;
-            a.cell_start = cs.get();
-            a.sorted_ids = sid.get();
             sxy.alloc(m, s);
             interleave_xy(sx.get(), sy.get(), m, sxy.get(), s);
-            a.sorted_xy = sxy.get();
-            a.perm = perm.get();
-            a.qcell = qcell.get();
-            run_knn_grid(a, s);
+            knn_grid_stage(qx, qy, n, *cfg, cs.get(), sid.get(), sxy.get(), m, k, k_eff, d2_out,
+                           idx_out, avg_out, s);
         } else {
+            FailFlags fails(s);
+            DBuf<double> dqx, dqy, d2(n * static_cast<size_t>(k_eff), s), avg(n, s);
+            DBuf<uint32_t> ids(idx_out ? n * static_cast<size_t>(k_eff) : 0, s);
+            DBuf<double> ddx, ddy;
+            h2d(dqx, qx, n, s);
+            h2d(dqy, qy, n, s);
             h2d(ddx, dx, m, s);
             h2d(ddy, dy, m, s);
+            KnnArgs a;
+            a.qx = dqx.get();
+            a.qy = dqy.get();
+            a.n = n;
+            a.m = m;
+            a.k = k;
+            a.k_eff = k_eff;
+            a.d2_out = d2.get();
+            a.id_out = idx_out ? ids.get() : nullptr;
+            a.avg_out = avg.get();
             a.dx = ddx.get();
             a.dy = ddy.get();
             run_knn_brute(a, s);
+            d2h(d2_out, d2.get(), n * static_cast<size_t>(k_eff), s);
+            if (idx_out) d2h(idx_out, ids.get(), n * static_cast<size_t>(k_eff), s);
+            d2h(avg_out, avg.get(), n, s);
         }
-        d2h(d2_out, d2.get(), n * static_cast<size_t>(k_eff), s);
-        if (idx_out) d2h(idx_out, ids.get(), n * static_cast<size_t>(k_eff), s);
-        d2h(avg_out, avg.get(), n, s);
         ss.sync();
     });
 }
+
+int aidw_build_index_mirror(const double* xs, const double* ys, size_t m,
+                            const aidw_grid_config* cfg, uint32_t* sorted_ids,
+                            uint32_t* cell_start, double* sorted_x, double* sorted_y,
+                            aidw_index** mirror, aidw_error* err) {
+    if (mirror) *mirror = nullptr;
+    return guarded(err, [&] {
+        build_index_checks(m, cfg);
+        auto h = std::make_unique<aidw_index>();
+        h->dev = current_device();
+        h->cfg = *cfg;
+        h->m = m;
+        CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+        cudaStream_t s = h->s;
+        {
+            FailFlags fails(s);
+            DBuf<double> dx, dy;
+            h2d(dx, xs, m, s);
+            h2d(dy, ys, m, s);
+            build_grid_device(dx.get(), dy.get(), m, *cfg, h->g, fails.slot(kFailData), s, true);
+            fails.fetch(s);
+            if (fails.h[kFailData] != LLONG_MAX) {
+                const long long i = fails.h[kFailData];
+                throw Failure(AIDW_ERR_DOMAIN, locate_msg(xs[i], ys[i]), i);
+            }
+            d2h(sorted_ids, h->g.sorted_ids.get(), m, s);
+            d2h(cell_start, h->g.cell_start.get(), h->g.cells + 1, s);
+            d2h(sorted_x, h->g.sorted_x.get(), m, s);
+            d2h(sorted_y, h->g.sorted_y.get(), m, s);
+            CK(cudaStreamSynchronize(s));
+        }
+        // the kNN kernel reads only cell_start, sorted_ids and the interleaved
+        // coordinates: the split copies go back to the pool
+        h->g.sorted_x.release();
+        h->g.sorted_y.release();
+        CK(cudaStreamSynchronize(s));
+        if (mirror) *mirror = h.release();
+    });
+}
+
+void aidw_index_release(aidw_index* mirror) { delete mirror; }
+
+int aidw_index_info(const aidw_index* mirror, aidw_grid_config* cfg, size_t* m) {
+    if (!mirror) return AIDW_ERR_INVALID_ARGUMENT;
+    if (cfg) *cfg = mirror->cfg;
+    if (m) *m = mirror->m;
+    return AIDW_OK;
+}
+
+int aidw_knn_stage_mirror(const double* qx, const double* qy, size_t n, const aidw_index* mirror,
+                          int32_t k, double* d2_out, uint32_t* idx_out, double* avg_out,
+                          int32_t* k_eff_out, int32_t* exhausted_out, aidw_error* err) {
+    return guarded(err, [&] {
+        if (!mirror) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "knn_stage: grid engine requires a grid index");
+        const size_t m = mirror->m;
+        const int k_eff = knn_stage_prologue(n, m, k, true, k_eff_out, exhausted_out);
+        if (n == 0) return;
+        DeviceScope on(mirror->dev);
+        StreamScope ss;
+        knn_grid_stage(qx, qy, n, mirror->cfg, mirror->g.cell_start.get(), mirror->g.sorted_ids.get(),
+                       mirror->g.sorted_xy.get(), m, k, k_eff, d2_out, idx_out, avg_out, ss.s);
+        ss.sync();
+    });
+}
+
+void* aidw_pinned_alloc(size_t bytes) { return pinned_alloc(bytes); }
+void aidw_pinned_free(void* p) { pinned_free(p); }
 
 int aidw_aidw_predict_all(const double* qx, const double* qy, size_t n, const double* dx,
                           const double* dy, const double* dz, size_t m, const double* r_obs,
@@ -1295,6 +1709,7 @@ int aidw_run_pipeline(const double* dx, const double* dy, const double* dz, size
         }
         StreamScope ss;
         cudaStream_t s = ss.s;
+        ArenaScope arena(s);  // uploads in the call's workspace too (graph-replayable)
         DBuf<double> ddx, ddy, ddz, dqx, dqy, pred(n, s), alpha(n, s);
         h2d(ddx, dx, m, s);
         h2d(ddy, dy, m, s);
@@ -1351,6 +1766,7 @@ int aidw_run_raster(const double* dx, const double* dy, const double* dz, size_t
         }
         StreamScope ss;
         cudaStream_t s = ss.s;
+        ArenaScope arena(s);  // uploads and lattice in the call's workspace too
         const size_t n = nx * ny;
         DBuf<double> ddx, ddy, ddz, dqx(n, s), dqy(n, s), pred(n, s), alpha(n, s);
         h2d(ddx, dx, m, s);

@@ -34,12 +34,29 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 // Every kernel launch of the library goes through LAUNCH so the launch
 // counter (aidw_kernel_launch_count, bench.py's gpu_launches) is exact.
 extern std::atomic<long long> g_launches;
+// While a pass is being captured into a CUDA graph its launches are counted
+// here (they run when the graph is launched, and are counted then).
+extern thread_local long long* t_launch_sink;
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                                   \
     do {                                                                                 \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                      \
-        ::aidwb::g_launches.fetch_add(1, std::memory_order_relaxed);                     \
+        if (::aidwb::t_launch_sink) ++*::aidwb::t_launch_sink;                            \
+        else ::aidwb::g_launches.fetch_add(1, std::memory_order_relaxed);                \
         CK(cudaGetLastError());                                                          \
     } while (0)
+
+// Timing event on a stream.  During CUDA-graph capture it becomes an
+// external event-record node (so graph replays still time); the external
+// flag is rejected outside capture, so it is used only then.
+inline void record_event(cudaEvent_t e, cudaStream_t s) {
+    if (!e) return;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s, &st));
+    if (st == cudaStreamCaptureStatusActive)
+        CK(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+    else
+        CK(cudaEventRecord(e, s));
+}
 
 // ------------------------------------------------------------------ workspace
 // Stream-ordered device buffers.  Inside a pipeline call (ArenaScope in
@@ -52,6 +69,7 @@ extern std::atomic<long long> g_launches;
 struct Arena {
     char* base = nullptr;
     size_t cap = 0, used = 0, overflow = 0;
+    unsigned small = 0;  // consecutive calls that used < 1/8 of a large workspace
     cudaStream_t stream = nullptr;
 };
 extern thread_local Arena* t_arena;

@@ -534,6 +534,17 @@ __device__ __forceinline__ f2 exp2_fma2(f2 x) {
                __int_as_float(__float_as_int(phi) + (__float_as_int(thi) << 23)));
 }
 
+__device__ __forceinline__ f2 lg2_2(f2 v) {
+    float lo, hi;
+    up2(v, lo, hi);
+    return pk2(mufu_lg2(lo), mufu_lg2(hi));
+}
+__device__ __forceinline__ f2 ex2_2(f2 v) {
+    float lo, hi;
+    up2(v, lo, hi);
+    return pk2(mufu_ex2(lo), mufu_ex2(hi));
+}
+
 // Per-thread query state: QT queries as QT/2 f32x2 pairs.
 // The coordinates are re-read per tile (L1-resident, 4 x 16 B per thread per
 // 256-point tile) instead of being held across the tile loop: the far pass
@@ -683,6 +694,31 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
                     sw[r] = add2(sw[r], w3);
                     swz[r] = fma2(w3, bc2(Z.w), swz[r]);
                 }
+            } else if (MODE == 1) {
+                // general alpha, exp2 split by point slot: of every 8 points
+                // of the far loop, slots 0-2 take MUFU.EX2 and 3-7 the FMA-pipe
+                // polynomial (both ~2e-7 relative) — 3 x 2 MUFU + 5 x 1 MUFU per
+                // 8 points balances the XU and FMA pipes (~44 vs 48 cycles per
+                // 4 query-points with half the queries all-MUFU).  The choice
+                // depends on the point's slot in its tile only: a function of
+                // the (query, point) pair, whatever warp the query is in.
+                const f2 e0 = fma2(q.c[r], lg2_2(d0), q.b[r]);
+                const f2 e1 = fma2(q.c[r], lg2_2(d1), q.b[r]);
+                const f2 e2 = fma2(q.c[r], lg2_2(d2), q.b[r]);
+                const f2 e3 = fma2(q.c[r], lg2_2(d3), q.b[r]);
+                const bool mufu = (j & 7) == 0;  // points j, j+1, j+2 of an 8-point slot
+                const f2 w0 = mufu ? ex2_2(e0) : exp2_fma2(e0);
+                const f2 w1 = mufu ? ex2_2(e1) : exp2_fma2(e1);
+                const f2 w2 = mufu ? ex2_2(e2) : exp2_fma2(e2);
+                const f2 w3 = exp2_fma2(e3);
+                sw[r] = add2(sw[r], w0);
+                swz[r] = fma2(w0, bc2(Z.x), swz[r]);
+                sw[r] = add2(sw[r], w1);
+                swz[r] = fma2(w1, bc2(Z.y), swz[r]);
+                sw[r] = add2(sw[r], w2);
+                swz[r] = fma2(w2, bc2(Z.z), swz[r]);
+                sw[r] = add2(sw[r], w3);
+                swz[r] = fma2(w3, bc2(Z.w), swz[r]);
             } else {
                 const f2 w0 = general_w<MODE, QT>(d0, q, r);
                 sw[r] = add2(sw[r], w0);
@@ -1049,6 +1085,7 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
 }  // namespace
 
 void set_alpha4_recipe(bool enabled) { g_alpha4_recipe.store(enabled); }
+bool alpha4_recipe_enabled() { return g_alpha4_recipe.load(); }
 
 namespace {
 std::atomic<size_t> g_query_slab{0};
@@ -1141,7 +1178,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     // a G1 / G2 interleave runs as all-G2 warps (AIDW_K4_G2 to tune)
     static const unsigned g2_threshold = [] {
         const char* v = std::getenv("AIDW_K4_G2");
-        const double share = v ? std::atof(v) : 0.5;
+        const double share = v ? std::atof(v) : 0.0;
         return static_cast<unsigned>(std::fmin(share, 1.0) * 4294967295.0);
     }();
     LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f,
@@ -1183,7 +1220,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     const int shape = variant != 0 ? variant : (ctas4 < static_cast<size_t>(16 * 148 * 2) ? 2 : 0);
     // (with several slabs the K4 events also bracket the settles between
     // them: ~1e-4 of a K4 slab)
-    if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+    if (times && times->k4_begin) record_event(times->k4_begin, s);
     for (size_t s0 = 0; s0 < q.n; s0 += slab) {
         ka.s0 = s0;
         ka.s1 = std::min(q.n, s0 + slab);
@@ -1194,7 +1231,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
             case 4: launch(weight_fp32_kernel<2, 3>, 2); break;
             default: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;
         }
-        if (times && times->k4_end && ka.s1 == q.n) CK(cudaEventRecord(times->k4_end, s));
+        if (times && times->k4_end && ka.s1 == q.n) record_event(times->k4_end, s);
         LAUNCH(settle_kernel, ceil_div(ka.s1 - ka.s0, kThreads), kThreads, 0, s, q, f, d,
                order_q.get(), part.get(), lshift.get(), sp.chunks, ka.s0, ka.s1, d_pred, d_alpha);
     }

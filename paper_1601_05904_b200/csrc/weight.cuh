@@ -80,6 +80,7 @@ constexpr int kWeightTile = 256;
 
 // Global switch of the alpha == 4 one-MUFU recipe (aidw_set_alpha4_recipe).
 void set_alpha4_recipe(bool enabled);
+bool alpha4_recipe_enabled();
 
 // Queries per weighting launch (K4 + settle): bounds the FP64 partial sums
 // to slab x chunks x 16 B whatever n is (aidw_set_query_slab; 0 = default,

@@ -155,9 +155,12 @@ __global__ void __launch_bounds__(kFp64Threads) weight_fp64_kernel(const WeightQ
                 for (int i = 0; i < QT; ++i) {
                     const double d2 = dsq_rn(qx[i], qy[i], xy.x, xy.y);
                     // d2^2 overflowing to inf weighs 0, as 1 / pow(sqrt(d2), 4)
-                    // does in the reference (rcp_nr(inf) would give NaN)
+                    // does in the reference (rcp_nr(inf) would give NaN); the
+                    // test runs on the integer pipe (a4 >= 0: inf <=> bits >=
+                    // those of inf), off the saturated FP64 pipe
                     const double a4 = __dmul_rn(d2, d2);
-                    const double w = a4 < INFINITY ? rcp_nr(a4) : 0.0;
+                    const double w =
+                        __double_as_longlong(a4) < 0x7FF0000000000000LL ? rcp_nr(a4) : 0.0;
                     if (BLOCKED) {
                         cw[i] = __dadd_rn(cw[i], w);
                         cwz[i] = __dadd_rn(cwz[i], __dmul_rn(w, z));
@@ -277,7 +280,7 @@ void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFra
         const dim3 grid(ceil_div(s1 - s0, static_cast<size_t>(kFp64Threads * k)), chunks);
         LAUNCH(kernel, grid, kFp64Threads, 0, s, q, d, order.get(), chunk_pts, s0, s1, part.get());
     };
-    if (times && times->k4_begin) CK(cudaEventRecord(times->k4_begin, s));
+    if (times && times->k4_begin) record_event(times->k4_begin, s);
     for (s0 = 0; s0 < q.n; s0 += slab) {
         s1 = std::min(q.n, s0 + slab);
         if (blocked) {
@@ -289,7 +292,7 @@ void weighting_fp64(const WeightQueries& q, const WeightData& d, const WeightFra
             else if (qt == 2) go(weight_fp64_kernel<false, 2>, 2);
             else go(weight_fp64_kernel<false, 1>, 1);
         }
-        if (times && times->k4_end && s1 == q.n) CK(cudaEventRecord(times->k4_end, s));
+        if (times && times->k4_end && s1 == q.n) record_event(times->k4_end, s);
         LAUNCH(fp64_settle_kernel, ceil_div(s1 - s0, kThreads), kThreads, 0, s, q, f, d,
                order.get(), part.get(), chunks, s0, s1, d_pred, d_alpha);
     }

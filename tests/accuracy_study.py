@@ -28,7 +28,7 @@ ap.add_argument("--general", action="store_true")
 ap.add_argument("--sample", type=int, default=1024)
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
-data, q = bench.make_inputs(A, cfg, 1, 0)
+data, q = bench.lib_inputs(A, cfg)
 if args.general:
     A.set_alpha4_recipe(False)
 out = A.run_pipeline(data, q, A.RunConfig(params=A.AidwParams(k=cfg["k"])))

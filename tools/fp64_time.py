@@ -3,7 +3,7 @@ sys.path.insert(0, '.')
 import bench, paper_1601_05904_b200 as A
 for cfgname, variant in [(c, v) for c in sys.argv[1:] or ["100k"] for v in ("blocked", "naive")]:
     cfg = bench.CONFIGS[cfgname]
-    data, q = bench.make_inputs(A, cfg, 1, 0)
+    data, q = bench.lib_inputs(A, cfg)
     A.set_weight_precision("fp64")
     for i in range(2):
         out = A.run_pipeline(data, q, A.RunConfig(params=A.AidwParams(k=cfg["k"]), variant=variant))

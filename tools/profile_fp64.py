@@ -17,7 +17,7 @@ ap.add_argument("--variant", default="blocked", choices=["blocked", "naive"])
 ap.add_argument("--passes", type=int, default=1)
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
-data, q = bench.make_inputs(A, cfg, 1, 0)
+data, q = bench.lib_inputs(A, cfg)
 A.set_weight_precision("fp64")
 for _ in range(args.passes):
     out = A.run_pipeline(data, q, A.RunConfig(params=A.AidwParams(k=cfg["k"]), variant=args.variant))

@@ -17,7 +17,7 @@ ap.add_argument("--general", action="store_true", help="force the general exp2/l
 ap.add_argument("--passes", type=int, default=2)
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
-data, q = bench.make_inputs(A, cfg, 1, 0)
+data, q = bench.lib_inputs(A, cfg)
 if args.general:
     A.set_alpha4_recipe(False)
 for i in range(args.passes):
