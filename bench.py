@@ -380,6 +380,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp64", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--verify", action="store_true",
+                    help="check the gathered shards against one device's run of all queries")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -453,14 +455,16 @@ def main():
             bb = shard.global_bbox(bb, dist if world > 1 else None,
                                    device=dev if not shared else None)
             self.rc = A.RunConfig(params=A.AidwParams(k=cfg["k"]), bbox=tuple(float(v) for v in bb))
+            self.rc_c = self.rc.c()
+            self.pp, self.pa = self.d_pred.data_ptr(), self.d_alpha.data_ptr()
 
         def step(self):
+            """One pass; returns the raw C stats (converted after timing)."""
             if lattice:  # cmd_raster: this rank's lattice rows generated in HBM each step
                 A.raster_lattice_device(LATTICE, self.ny, self.lbox, self.qx, self.qy, self.r0,
                                         self.rows, self.sp)
             return A.run_pipeline_device(self.dx, self.dy, self.dz, self.m, self.qx, self.qy,
-                                         self.n, self.rc, self.d_pred.data_ptr(),
-                                         self.d_alpha.data_ptr(), self.sp)
+                                         self.n, self.rc_c, self.pp, self.pa, self.sp, raw=True)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -482,7 +486,7 @@ def main():
         barrier()
         launches = A.kernel_launch_count() - l0
         step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-        return allmax(sum(step_ms)) / steps, stats, launches
+        return allmax(sum(step_ms)) / steps, [st.as_dict() for st in stats], launches
 
     job = Job(scaling)
     m, n = job.m, job.n
@@ -531,7 +535,7 @@ def main():
     gen_stats = []
     for _ in range(2):
         flush.zero_()
-        gen_stats.append(job.step())
+        gen_stats.append(job.step().as_dict())
     A.set_alpha4_recipe(True)
     k4g_ms = statistics.median(s["weight_kernel_ms"] for s in gen_stats)
     torch.cuda.synchronize()
@@ -545,6 +549,37 @@ def main():
         fp64 = {"value": job.n_total / (ms64 / 1e3), "unit": "points/s", "ms_per_step": ms64,
                 "k4_ms": statistics.median(s["weight_kernel_ms"] for s in st64),
                 "kernel": "weight_fp64_kernel<BLOCKED> (AIDW_WEIGHT_FP64=1)"}
+
+    # --verify: the ranks' shards, gathered, equal one device's run of the
+    # whole query set bit for bit (the invariance the sharding relies on)
+    verify = None
+    if args.verify and scaling == "strong":
+        job.step()
+        torch.cuda.synchronize()
+        mine = torch.stack([job.d_pred, job.d_alpha]).cpu()
+        if world > 1:
+            parts = [None] * world
+            dist.all_gather_object(parts, mine)
+        else:
+            parts = [mine]
+        if rank == 0:
+            got = torch.cat(parts, dim=1)
+            (dxs_, dys_, dzs_), (qxs_, qys_) = make_inputs(gen, cfg, 1, 0, "strong")
+            d_all = torch.from_numpy(np.stack([dxs_, dys_, dzs_])).to(dev)
+            q_all = torch.from_numpy(np.stack([qxs_, qys_])).to(dev)
+            p_all = torch.empty(qxs_.size, dtype=torch.float64, device=dev)
+            a_all = torch.empty(qxs_.size, dtype=torch.float64, device=dev)
+            if lattice:
+                A.raster_lattice_device(LATTICE, LATTICE, job.lbox, q_all[0].data_ptr(),
+                                        q_all[1].data_ptr(), 0, LATTICE, job.sp)
+            A.run_pipeline_device(d_all[0].data_ptr(), d_all[1].data_ptr(), d_all[2].data_ptr(),
+                                  dxs_.size, q_all[0].data_ptr(), q_all[1].data_ptr(), qxs_.size,
+                                  job.rc, p_all.data_ptr(), a_all.data_ptr(), job.sp)
+            torch.cuda.synchronize()
+            ref = torch.stack([p_all, a_all]).cpu()
+            verify = {"shards_bit_identical": bool(torch.equal(got, ref)), "n": int(got.shape[1])}
+        if world > 1:
+            dist.barrier()
 
     # weak-scaling figure beside the strong one (N > 1): 1M queries per rank
     weak = None
@@ -650,12 +685,15 @@ def main():
                     "d2h_bytes_per_step": (8 if raster_e2e else 16) * n,
                     "s_per_step": e2e_s},
             "gpu_launches": launches,
+            "cuda_graphs": A.graph_counters(),
             "clocks": clk,
         }
         if fp64 is not None:
             line["fp64"] = fp64
         if weak is not None:
             line["weak_scaling"] = weak
+        if verify is not None:
+            line["verify"] = verify
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")
                                     if k in cpu}

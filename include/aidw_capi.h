@@ -219,6 +219,12 @@ int32_t aidw_device_count(void);
  * distinct devices, cached) to the others; shards on one device share its
  * replica.  NCCL is dlopen'ed ("libnccl.so.2"); without it CUDA peer copies
  * fill the replicas.  Introspection for tests and logs: */
+/* CUDA-graph cache of fused passes (a pass with the plan, buffers and
+ * workspace of an earlier one is replayed as one graph launch; AIDW_GRAPHS=0
+ * or aidw_set_graphs(0) disables it): captures and replays so far. */
+void aidw_graph_counters(int64_t* captures, int64_t* replays);
+void aidw_set_graphs(int32_t enabled);
+
 int64_t aidw_nccl_broadcast_count(void); /* grouped broadcasts issued so far   */
 int32_t aidw_last_replication(void);     /* 0 none, 1 NCCL broadcast, 2 peer   */
 int32_t aidw_nccl_version(void);         /* NCCL_VERSION_CODE, 0 if unloadable */

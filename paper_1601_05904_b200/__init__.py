@@ -10,7 +10,7 @@ from .api import (  # noqa: F401
     AidwParams, AidwRuntimeError, BoundingBox, CudaError, DomainError, GridConfig, GridIndex,
     InterpolationResult, InvalidArgument, KnnStageResult, OutOfRange, PipelineOutcome, PointSet,
     Raster, RasterOutcome, RunConfig, aidw_predict_all, build_index, choose_cell_width,
-    compute_bbox, compute_bbox_device, device_count, device_info, generate_clustered, generate_random_points,
+    compute_bbox, compute_bbox_device, graph_counters, set_graphs, device_count, device_info, generate_clustered, generate_random_points,
     generate_random_queries, idw_predict_all, kernel_launch_count, knn_stage, make_grid_config,
     parse_raster_asc, raster_lattice, replication_info, raster_lattice_device, read_data_csv, read_query_csv,
     run_pipeline, run_pipeline_device, run_raster, set_alpha4_recipe, set_devices, set_query_slab,

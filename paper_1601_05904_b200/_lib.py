@@ -94,6 +94,8 @@ SIGNATURES = {
     "aidw_set_devices": (C.c_int, [_i32p, C.c_int32, _ep]),
     "aidw_device_count": (C.c_int32, []),
     "aidw_nccl_broadcast_count": (C.c_int64, []),
+    "aidw_graph_counters": (None, [_i64p, _i64p]),
+    "aidw_set_graphs": (None, [C.c_int32]),
     "aidw_last_replication": (C.c_int32, []),
     "aidw_nccl_version": (C.c_int32, []),
     "aidw_build_index": (C.c_int, [_dp, _dp, C.c_size_t, C.POINTER(GridConfig), _u32p, _u32p,

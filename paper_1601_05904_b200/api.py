@@ -254,6 +254,18 @@ def device_count() -> int:
     return int(lib().aidw_device_count())
 
 
+def graph_counters() -> dict:
+    """CUDA-graph cache of fused passes: captures and replays so far."""
+    c, r = C.c_int64(), C.c_int64()
+    lib().aidw_graph_counters(C.byref(c), C.byref(r))
+    return {"captures": int(c.value), "replays": int(r.value)}
+
+
+def set_graphs(enabled: bool):
+    """Enable / disable the CUDA-graph cache (results never depend on it)."""
+    lib().aidw_set_graphs(1 if enabled else 0)
+
+
 def replication_info() -> dict:
     """How the last multi-device run replicated the data: NCCL
     broadcasts issued so far, the last replication kind and NCCL's version."""
@@ -468,15 +480,17 @@ def run_pipeline(data: PointSet, queries: PointSet, cfg: RunConfig, out=None) ->
     return PipelineOutcome(InterpolationResult(pred, alph), st.as_dict(), int(st.k_effective))
 
 
-def run_pipeline_device(d_dx, d_dy, d_dz, m, d_qx, d_qy, n, cfg: RunConfig, d_pred, d_alpha,
-                        stream=None) -> dict:
-    """Device-resident pipeline over raw device pointers (ints); returns stats."""
+def run_pipeline_device(d_dx, d_dy, d_dz, m, d_qx, d_qy, n, cfg, d_pred, d_alpha,
+                        stream=None, raw=False):
+    """Device-resident pipeline over raw device pointers (ints); returns stats
+    (a dict, or with raw=True the C struct — convert later with .as_dict()).
+    `cfg` is a RunConfig or an already converted L.RunConfig (cfg.c())."""
     st = L.RunStats()
-    c = cfg.c()
+    c = cfg.c() if isinstance(cfg, RunConfig) else cfg
     err = L.Error()
     _raise(lib().aidw_run_pipeline_device(d_dx, d_dy, d_dz, m, d_qx, d_qy, n, C.byref(c), d_pred,
                                           d_alpha, C.byref(st), stream, C.byref(err)), err)
-    return st.as_dict()
+    return st if raw else st.as_dict()
 
 
 @dataclass

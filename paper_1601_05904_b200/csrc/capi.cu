@@ -114,18 +114,14 @@ double snap_sq_h(const Box& b) {  // interpolate.hpp:86-89
     return eps * eps;
 }
 
-WeightFrame make_frame(const Box& b, double zlo, double zhi) {
+// d_zhull: the device value hull {zlo, zhi} (the kernels derive zshift).
+WeightFrame make_frame(const Box& b, const double* d_zhull) {
     WeightFrame f;
     f.ox = b.min_x;
     f.oy = b.min_y;
     const double span = std::max(b.width(), b.height());
     f.inv_scale = (span > 0.0 && std::isfinite(span)) ? 1.0 / span : 1.0;
-    const double zmax = std::max(std::fabs(zlo), std::fabs(zhi));
-    int e = 0;
-    if (zmax > 0.0 && std::isfinite(zmax)) std::frexp(zmax, &e);
-    f.zshift = -e;  // |z * 2^zshift| < 1
-    f.zlo = zlo;
-    f.zhi = zhi;
+    f.zhull = d_zhull;
     f.snap_sq = snap_sq_h(b);
     return f;
 }
@@ -229,18 +225,25 @@ void d2h(T* dst, const T* src, size_t n, cudaStream_t s) {
 }
 
 // bbox of (a ∪ b) plus the z hull, device reduce -> host.
+// d_out6 = {min_x, min_y, max_x, max_y, zlo, zhi} of (a ∪ b) and z.
 struct Extents {
     Box box;
-    double zlo, zhi;
+    const double* d_hull = nullptr;  // device, 6 doubles; zhull = d_hull + 4
 };
-Extents extents(const double* ax, const double* ay, size_t na, const double* bx, const double* by,
-                size_t nb, const double* z, size_t nz, cudaStream_t s) {
-    DBuf<double> out(6, s);
-    bbox_reduce_device(ax, ay, na, bx, by, nb, z, nz, out.get(), s);
+// Device reduce into d_out6, then (one host round trip) the box.
+Extents extents(double* d_out6, const double* ax, const double* ay, size_t na, const double* bx,
+                const double* by, size_t nb, const double* z, size_t nz, cudaStream_t s) {
+    bbox_reduce_device(ax, ay, na, bx, by, nb, z, nz, d_out6, s);
     double h[6];
-    d2h(h, out.get(), 6, s);
+    d2h(h, d_out6, 6, s);
     CK(cudaStreamSynchronize(s));
-    return Extents{Box{h[0], h[1], h[2], h[3]}, h[4], h[5]};
+    return Extents{Box{h[0], h[1], h[2], h[3]}, d_out6};
+}
+// Host box only (the device result is dropped with the call).
+Box extents_box(const double* ax, const double* ay, size_t na, const double* bx,
+                const double* by, size_t nb, cudaStream_t s) {
+    DBuf<double> out(6, s);
+    return extents(out.get(), ax, ay, na, bx, by, nb, nullptr, 0, s).box;
 }
 
 // Slots 0-2: failure indices (LLONG_MAX = none); 3-5: counters (0).
@@ -362,7 +365,7 @@ void weighting_stage(const double* d_dx, const double* d_dy, const double* d_dz,
                      const double* d_qx, const double* d_qy, size_t n, const double* d_alpha_q,
                      const Extents& ext, WeightMode mode, double* d_pred, double* d_alpha_out,
                      FailFlags& fails, WeightTimes* wt, cudaStream_t s) {
-    const WeightFrame frame = make_frame(ext.box, ext.zlo, ext.zhi);
+    const WeightFrame frame = make_frame(ext.box, ext.d_hull + 4);
     WeightData wd{d_dx, d_dy, d_dz, m};
     // snap index, nearest index and d2_min per query (k = 1 grid search,
     // FP64): the weighting kernels' snap rule and non-finite fallback
@@ -452,12 +455,14 @@ struct PassPlan {
     WeightFrame frame{};
     bool own_g4 = false;  // K4 record order from a separate factor-4 grid
     aidw_grid_config g4c{};
+    double* d_hull = nullptr;   // device {bbox, zlo, zhi}
+    bool hull_in_pass = false;  // reduce the value hull as the pass's first step
 };
 
 // Validation + extents (the one host round trip before the pass) + set-up
 // (cli.hpp:217-268, with the reference's exception order).
 PassPlan plan_pass(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_stats* st,
-                   cudaStream_t s) {
+                   double* d_hull, cudaStream_t s) {
     if (cfg.workers < 0)
         throw Failure(AIDW_ERR_INVALID_ARGUMENT, "resolve_workers: worker count must be >= 0");
     const size_t m = io.m, n = io.n;
@@ -465,14 +470,16 @@ PassPlan plan_pass(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
     if (!io.dz) throw Failure(AIDW_ERR_INVALID_ARGUMENT, "interpolation: data set carries no values");
     PassPlan pl;
     pl.wmode = weight_mode(cfg.variant, 0);
-    // bbox(data ∪ queries) and the value hull
+    // bbox(data ∪ queries) and the value hull.  A given bbox needs no host
+    // round trip: the value hull is reduced inside the pass (device only).
     if (cfg.use_bbox) {
-        pl.ext = extents(nullptr, nullptr, 0, nullptr, nullptr, 0, io.dz, m, s);
-        pl.ext.box = Box{cfg.bbox[0], cfg.bbox[1], cfg.bbox[2], cfg.bbox[3]};
+        pl.ext = Extents{Box{cfg.bbox[0], cfg.bbox[1], cfg.bbox[2], cfg.bbox[3]}, d_hull};
+        pl.hull_in_pass = true;
     } else {
-        pl.ext = extents(io.dx, io.dy, m, io.qx, io.qy, n, io.dz, m, s);
+        pl.ext = extents(d_hull, io.dx, io.dy, m, io.qx, io.qy, n, io.dz, m, s);
     }
-    pl.frame = make_frame(pl.ext.box, pl.ext.zlo, pl.ext.zhi);
+    pl.d_hull = d_hull;
+    pl.frame = make_frame(pl.ext.box, d_hull + 4);
     if (cfg.mode == AIDW_MODE_IDW) {
         if (!(cfg.alpha > 0.0) || !std::isfinite(cfg.alpha))
             throw Failure(AIDW_ERR_INVALID_ARGUMENT, "idw_predict_all: alpha must be positive finite");
@@ -517,6 +524,8 @@ PassPlan plan_pass(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_st
 void enqueue_pass(const PassPlan& pl, const PipelineIO& io, const aidw_run_config& cfg,
                   const PassEvents& pe, FailFlags& fails, cudaStream_t s) {
     const size_t m = io.m, n = io.n;
+    if (pl.hull_in_pass)
+        bbox_reduce_device(nullptr, nullptr, 0, nullptr, nullptr, 0, io.dz, m, pl.d_hull, s);
     WeightTimes wt;
     wt.k4_begin = pe.k4b;
     wt.k4_end = pe.k4e;
@@ -766,7 +775,7 @@ std::vector<unsigned char> graph_key(const PipelineIO& io, const aidw_run_config
     std::memcpy(k.ptr, p, sizeof p);
     k.cfg = cfg;
     const double e[6] = {pl.ext.box.min_x, pl.ext.box.min_y, pl.ext.box.max_x, pl.ext.box.max_y,
-                         pl.ext.zlo, pl.ext.zhi};
+                         pl.hull_in_pass ? 1.0 : 0.0, 0.0};
     std::memcpy(k.ext, e, sizeof e);
     (void)s;
     std::vector<unsigned char> out(sizeof k);
@@ -873,7 +882,8 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
     const long long launches0 = g_launches.load();
     MaybeArena arena(s);  // declared first: destroyed after every DBuf of the call
     aidw_run_stats local{};
-    const PassPlan pl = plan_pass(io, cfg, &local, s);
+    DBuf<double> hull(6, s);
+    const PassPlan pl = plan_pass(io, cfg, &local, hull.get(), s);
     FailFlags fails(s, /*defer_init=*/true);
     PassEvents eager;
     struct EventsGuard {
@@ -1101,11 +1111,10 @@ struct PipelineShards {
         h2d(b[d].qy, qy + lo, hi - lo, s);
         b[d].pred.alloc(hi - lo, s);
         b[d].alpha.alloc(hi - lo, s);
-        const Extents e =
-            extents(b[d].dx, b[d].dy, m, b[d].qx.get(), b[d].qy.get(), hi - lo, nullptr, 0, s);
+        const Box e = extents_box(b[d].dx, b[d].dy, m, b[d].qx.get(), b[d].qy.get(), hi - lo, s);
         b[d].h2d_ms +=
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
-        return e.box;
+        return e;
     }
     void run(size_t d, cudaStream_t s, const Box& g) {
         size_t lo, hi;
@@ -1157,8 +1166,7 @@ struct RasterShards {
     aidw_run_stats* st;
 
     Box prep(size_t d, cudaStream_t s) {
-        const Extents e = extents(b[d].dx, b[d].dy, m, nullptr, nullptr, 0, nullptr, 0, s);
-        return e.box;
+        return extents_box(b[d].dx, b[d].dy, m, nullptr, nullptr, 0, s);
     }
     void run(size_t d, cudaStream_t s, const Box& g) {
         size_t r0, r1;
@@ -1587,7 +1595,9 @@ int aidw_aidw_predict_all(const double* qx, const double* qy, size_t n, const do
         h2d(dqx, qx, n, s);
         h2d(dqy, qy, n, s);
         h2d(drobs, r_obs, n, s);
-        const Extents ext = extents(ddx.get(), ddy.get(), m, dqx.get(), dqy.get(), n, ddz.get(), m, s);
+        DBuf<double> hull(6, s);
+        const Extents ext =
+            extents(hull.get(), ddx.get(), ddy.get(), m, dqx.get(), dqy.get(), n, ddz.get(), m, s);
         const double area = params->area > 0.0 ? params->area : ext.box.area();
         // adaptive_alpha's host-checkable preconditions, first failing query
         // (adaptive.hpp:101-112): size, area, r_exp, r_obs sign.
@@ -1658,7 +1668,9 @@ int aidw_idw_predict_all(const double* qx, const double* qy, size_t n, const dou
         h2d(ddz, dz, m, s);
         h2d(dqx, qx, n, s);
         h2d(dqy, qy, n, s);
-        const Extents ext = extents(ddx.get(), ddy.get(), m, dqx.get(), dqy.get(), n, ddz.get(), m, s);
+        DBuf<double> hull(6, s);
+        const Extents ext =
+            extents(hull.get(), ddx.get(), ddy.get(), m, dqx.get(), dqy.get(), n, ddz.get(), m, s);
         LAUNCH(fill_f64_kernel, ceil_div(n, kThreads), kThreads, 0, s, alpha_q.get(), n, alpha);
         weighting_stage(ddx.get(), ddy.get(), ddz.get(), m, dqx.get(), dqy.get(), n,
                         alpha_q.get(), ext, weight_mode(variant, pinned_order), pred.get(),
@@ -1689,6 +1701,12 @@ int32_t aidw_device_count(void) {
     const auto d = device_list();
     return static_cast<int32_t>(d.size() > 1 ? d.size() : 1);
 }
+
+void aidw_graph_counters(int64_t* captures, int64_t* replays) {
+    if (captures) *captures = g_graph_captures.load();
+    if (replays) *replays = g_graph_replays.load();
+}
+void aidw_set_graphs(int32_t enabled) { g_graphs_enabled.store(enabled != 0 ? 1 : 0); }
 
 int64_t aidw_nccl_broadcast_count(void) { return nccl_broadcast_count(); }
 int32_t aidw_last_replication(void) { return last_replication_kind(); }
@@ -1777,8 +1795,8 @@ int aidw_run_raster(const double* dx, const double* dy, const double* dz, size_t
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         // the lattice spans bbox(data) (cli.hpp:495); its cell centres lie
         // inside it, so bbox(data ∪ lattice) is the same box
-        const Extents e = extents(ddx.get(), ddy.get(), m, nullptr, nullptr, 0, nullptr, 0, s);
-        const double bb[4] = {e.box.min_x, e.box.min_y, e.box.max_x, e.box.max_y};
+        const Box eb = extents_box(ddx.get(), ddy.get(), m, nullptr, nullptr, 0, s);
+        const double bb[4] = {eb.min_x, eb.min_y, eb.max_x, eb.max_y};
         if (bbox_out) std::memcpy(bbox_out, bb, sizeof bb);
         lattice_device(nx, ny, bb, 0, ny, dqx.get(), dqy.get(), s);
         aidw_run_config c = *cfg;
@@ -1797,11 +1815,11 @@ int aidw_compute_bbox_device(const double* d_dx, const double* d_dy, size_t m,
         if (m == 0 && n == 0)
             throw Failure(AIDW_ERR_INVALID_ARGUMENT, "compute_bbox: both point sets are empty");
         StreamScope ss(stream);
-        const Extents e = extents(d_dx, d_dy, m, d_qx, d_qy, n, nullptr, 0, ss.s);
-        out[0] = e.box.min_x;
-        out[1] = e.box.min_y;
-        out[2] = e.box.max_x;
-        out[3] = e.box.max_y;
+        const Box e = extents_box(d_dx, d_dy, m, d_qx, d_qy, n, ss.s);
+        out[0] = e.min_x;
+        out[1] = e.min_y;
+        out[2] = e.max_x;
+        out[3] = e.max_y;
     });
 }
 

@@ -144,9 +144,10 @@ static_assert(kComps * kWeightTile == kTileFloats, "tile layout");
 __global__ void prep_data_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                  const double* __restrict__ z, const uint32_t* __restrict__ order,
                                  size_t m, size_t mp, double ox, double oy, double inv_scale,
-                                 double zmul, float* __restrict__ rec) {
+                                 const double* __restrict__ zhull, float* __restrict__ rec) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= mp) return;
+    const double zmul = ldexp(1.0, frame_zshift(zhull));
     float* r = rec + (i / kWeightTile) * kTileFloats + (i % kWeightTile);
     if (i < m) {
         const size_t j = order ? order[i] : i;
@@ -165,32 +166,43 @@ __global__ void prep_data_kernel(const double* __restrict__ x, const double* __r
     }
 }
 
-// One warp per tile: bounding box of the real records (hi parts), centre c,
+// One CTA per tile (a thread per record): bounding box of the real records
+// (hi parts), centre c,
 // near threshold, and the far-form components.  A (query, tile) pair is FAR
 // when the query's distance d to the box exceeds both R_far and 0.3 box
 // diagonals: then |q'| + |p'| <= d + diag <= 4.4 d, so the expanded d2 loses
 // at most a few ulp of 19 d2 (the measured contract error is unchanged from
 // a 0.5-diagonal rule: tools/accuracy sweeps in DESIGN.md).
 // Partial (padded) tiles are always NEAR.
-__global__ void tile_geo_kernel(float* __restrict__ rec, size_t m, size_t tiles, float rfar2,
-                                float diagf2, float4* __restrict__ box, float4* __restrict__ geo) {
-    const size_t tile = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (tile >= tiles) return;
+__global__ void __launch_bounds__(kWeightTile) tile_geo_kernel(float* __restrict__ rec, size_t m,
+                                                              size_t tiles, float rfar2, float diagf2,
+                                                              float4* __restrict__ box,
+                                                              float4* __restrict__ geo) {
+    // one CTA per tile, one thread per record
+    __shared__ float s_red[4][kWeightTile / 32];
+    const size_t tile = blockIdx.x;
+    const int j = threadIdx.x, lane = j & 31, warp = j >> 5;
     float* t = rec + tile * kTileFloats;
-    float x0 = 3.0e38f, y0 = 3.0e38f, x1 = -3.0e38f, y1 = -3.0e38f;
-    for (int j = lane; j < kWeightTile; j += 32) {
-        if (tile * kWeightTile + j < m) {
-            const float px = t[kXH * kWeightTile + j], py = t[kYH * kWeightTile + j];
-            x0 = fminf(x0, px), y0 = fminf(y0, py), x1 = fmaxf(x1, px), y1 = fmaxf(y1, py);
-        }
-    }
+    const bool real = tile * kWeightTile + j < m;
+    const float pxh = t[kXH * kWeightTile + j], pyh = t[kYH * kWeightTile + j];
+    float x0 = real ? pxh : 3.0e38f, y0 = real ? pyh : 3.0e38f;
+    float x1 = real ? pxh : -3.0e38f, y1 = real ? pyh : -3.0e38f;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         x0 = fminf(x0, __shfl_xor_sync(0xFFFFFFFFu, x0, o));
         y0 = fminf(y0, __shfl_xor_sync(0xFFFFFFFFu, y0, o));
         x1 = fmaxf(x1, __shfl_xor_sync(0xFFFFFFFFu, x1, o));
         y1 = fmaxf(y1, __shfl_xor_sync(0xFFFFFFFFu, y1, o));
+    }
+    if (lane == 0) {
+        s_red[0][warp] = x0, s_red[1][warp] = y0, s_red[2][warp] = x1, s_red[3][warp] = y1;
+    }
+    __syncthreads();
+    x0 = s_red[0][0], y0 = s_red[1][0], x1 = s_red[2][0], y1 = s_red[3][0];
+#pragma unroll
+    for (int w = 1; w < kWeightTile / 32; ++w) {
+        x0 = fminf(x0, s_red[0][w]), y0 = fminf(y0, s_red[1][w]);
+        x1 = fmaxf(x1, s_red[2][w]), y1 = fmaxf(y1, s_red[3][w]);
     }
     const float cx = 0.5f * (x0 + x1), cy = 0.5f * (y0 + y1);
     const float gx = x1 - x0, gy = y1 - y0;
@@ -201,25 +213,21 @@ __global__ void tile_geo_kernel(float* __restrict__ rec, size_t m, size_t tiles,
     const float thr2 =
         partial ? INFINITY : fmaxf(fmaxf(rfar2, 1.0e-8f), 1.001f * diagf2 * fmaf(gx, gx, gy * gy));
 #endif
-    if (lane == 0) {
+    if (j == 0) {
         box[tile] = make_float4(x0, y0, x1, y1);
         geo[tile] = make_float4(cx, cy, thr2, 0.0f);
     }
-    for (int j = lane; j < kWeightTile; j += 32) {
-        float px2 = 0.0f, py2 = 0.0f, pp = 0.0f;
-        if (tile * kWeightTile + j < m) {
-            const double px = (static_cast<double>(t[kXH * kWeightTile + j]) - cx) +
-                              static_cast<double>(t[kXL * kWeightTile + j]);
-            const double py = (static_cast<double>(t[kYH * kWeightTile + j]) - cy) +
-                              static_cast<double>(t[kYL * kWeightTile + j]);
-            px2 = __double2float_rn(-2.0 * px);
-            py2 = __double2float_rn(-2.0 * py);
-            pp = __double2float_rn(px * px + py * py);
-        }
-        t[kPX * kWeightTile + j] = px2;
-        t[kPY * kWeightTile + j] = py2;
-        t[kPP * kWeightTile + j] = pp;
+    float px2 = 0.0f, py2 = 0.0f, pp = 0.0f;
+    if (real) {
+        const double px = (static_cast<double>(pxh) - cx) + static_cast<double>(t[kXL * kWeightTile + j]);
+        const double py = (static_cast<double>(pyh) - cy) + static_cast<double>(t[kYL * kWeightTile + j]);
+        px2 = __double2float_rn(-2.0 * px);
+        py2 = __double2float_rn(-2.0 * py);
+        pp = __double2float_rn(px * px + py * py);
     }
+    t[kPX * kWeightTile + j] = px2;
+    t[kPY * kWeightTile + j] = py2;
+    t[kPP * kWeightTile + j] = pp;
 }
 
 std::atomic<bool> g_alpha4_recipe{true};
@@ -325,8 +333,11 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
     const size_t jz = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (jz >= q.n) return;
     const size_t p = zpos[jz];
+    // the five flag arrays are scanned as one concatenation: an array's
+    // exclusive scan is offset by its first value (the earlier arrays' total)
+    const uint32_t base_g2 = scan_g2[0];
     const size_t num_a = static_cast<size_t>(scan_a[q.n - 1]) + flag_a[q.n - 1];
-    const size_t num_g2 = static_cast<size_t>(scan_g2[q.n - 1]) + flag_g2[q.n - 1];
+    const size_t num_g2 = static_cast<size_t>(scan_g2[q.n - 1] - base_g2) + flag_g2[q.n - 1];
     const size_t num_g1 = q.n - num_a - num_g2;
     const bool is_a = flag_a[jz] != 0, is_g2 = flag_g2[jz] != 0;
     int sub = -1;  // recipe sub-class (-1: alpha = 4)
@@ -339,9 +350,10 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
         size_t cnt[kRecipeSubs], before = 0, total = 0;
 #pragma unroll
         for (int k = 0; k < kRecipeSubs; ++k) {
-            cnt[k] = static_cast<size_t>(rf.scan[k][q.n - 1]) + rf.flag[k][q.n - 1];
+            const uint32_t base = rf.scan[k][0];
+            cnt[k] = static_cast<size_t>(rf.scan[k][q.n - 1] - base) + rf.flag[k][q.n - 1];
             total += cnt[k];
-            before += rf.scan[k][jz];
+            before += rf.scan[k][jz] - base;
             if (rf.flag[k][jz]) sub = k;
         }
         size_t off = num_a - total;  // alpha = 4 count
@@ -349,10 +361,11 @@ __global__ void query_records_kernel(const WeightQueries q, WeightFrame f,
             i = num_g1 + num_g2 + (scan_a[jz] - before);
         } else {
             for (int k = 0; k < sub; ++k) off += cnt[k];
-            i = num_g1 + num_g2 + off + rf.scan[sub][jz];
+            i = num_g1 + num_g2 + off + (rf.scan[sub][jz] - rf.scan[sub][0]);
         }
     } else {
-        const size_t j = is_g2 ? scan_g2[jz] : jz - scan_a[jz] - scan_g2[jz];
+        const size_t sg2 = scan_g2[jz] - base_g2;
+        const size_t j = is_g2 ? sg2 : jz - scan_a[jz] - sg2;
         const size_t both = (num_g1 < num_g2 ? num_g1 : num_g2) / 64;  // full block pairs
         if (j < 64 * both) {
             i = (j / 64) * 128 + (is_g2 ? 64 : 0) + (j % 64);
@@ -534,17 +547,6 @@ __device__ __forceinline__ f2 exp2_fma2(f2 x) {
                __int_as_float(__float_as_int(phi) + (__float_as_int(thi) << 23)));
 }
 
-__device__ __forceinline__ f2 lg2_2(f2 v) {
-    float lo, hi;
-    up2(v, lo, hi);
-    return pk2(mufu_lg2(lo), mufu_lg2(hi));
-}
-__device__ __forceinline__ f2 ex2_2(f2 v) {
-    float lo, hi;
-    up2(v, lo, hi);
-    return pk2(mufu_ex2(lo), mufu_ex2(hi));
-}
-
 // Per-thread query state: QT queries as QT/2 f32x2 pairs.
 // The coordinates are re-read per tile (L1-resident, 4 x 16 B per thread per
 // 256-point tile) instead of being held across the tile loop: the far pass
@@ -694,31 +696,6 @@ __device__ __forceinline__ void k4_far(const float* __restrict__ t, const QState
                     sw[r] = add2(sw[r], w3);
                     swz[r] = fma2(w3, bc2(Z.w), swz[r]);
                 }
-            } else if (MODE == 1) {
-                // general alpha, exp2 split by point slot: of every 8 points
-                // of the far loop, slots 0-2 take MUFU.EX2 and 3-7 the FMA-pipe
-                // polynomial (both ~2e-7 relative) — 3 x 2 MUFU + 5 x 1 MUFU per
-                // 8 points balances the XU and FMA pipes (~44 vs 48 cycles per
-                // 4 query-points with half the queries all-MUFU).  The choice
-                // depends on the point's slot in its tile only: a function of
-                // the (query, point) pair, whatever warp the query is in.
-                const f2 e0 = fma2(q.c[r], lg2_2(d0), q.b[r]);
-                const f2 e1 = fma2(q.c[r], lg2_2(d1), q.b[r]);
-                const f2 e2 = fma2(q.c[r], lg2_2(d2), q.b[r]);
-                const f2 e3 = fma2(q.c[r], lg2_2(d3), q.b[r]);
-                const bool mufu = (j & 7) == 0;  // points j, j+1, j+2 of an 8-point slot
-                const f2 w0 = mufu ? ex2_2(e0) : exp2_fma2(e0);
-                const f2 w1 = mufu ? ex2_2(e1) : exp2_fma2(e1);
-                const f2 w2 = mufu ? ex2_2(e2) : exp2_fma2(e2);
-                const f2 w3 = exp2_fma2(e3);
-                sw[r] = add2(sw[r], w0);
-                swz[r] = fma2(w0, bc2(Z.x), swz[r]);
-                sw[r] = add2(sw[r], w1);
-                swz[r] = fma2(w1, bc2(Z.y), swz[r]);
-                sw[r] = add2(sw[r], w2);
-                swz[r] = fma2(w2, bc2(Z.z), swz[r]);
-                sw[r] = add2(sw[r], w3);
-                swz[r] = fma2(w3, bc2(Z.w), swz[r]);
             } else {
                 const f2 w0 = general_w<MODE, QT>(d0, q, r);
                 sw[r] = add2(sw[r], w0);
@@ -1063,6 +1040,8 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
             sw += v.x;
             swz += v.y;
         }
+        const int zshift = frame_zshift(f.zhull);
+        const double zlo = f.zhull[0], zhi = f.zhull[1];
         // The FP64 reference overflows / underflows where the true (unscaled)
         // weights do (interpolate.hpp:109-118): its largest weight is
         // 2^e, e = -alpha/2 log2 d2_min; its sums are 2^lshift * (sw, swz / 2^zshift).
@@ -1070,12 +1049,12 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
         const double sh = lshift[i];
         bool fallback = !(sw > 0.0) || !isfinite(sw) || !isfinite(swz) || !(e < 1024.0) ||
                         !(sh + log2(sw) < 1024.0) || e < -1075.0;
-        if (!fallback && swz != 0.0 && !(sh + log2(fabs(swz)) - f.zshift < 1024.0)) fallback = true;
+        if (!fallback && swz != 0.0 && !(sh + log2(fabs(swz)) - zshift < 1024.0)) fallback = true;
         if (fallback) {
             out = d.z[q.nn_s[p]];
         } else {
-            double v = ldexp(swz / sw, -f.zshift);
-            out = v < f.zlo ? f.zlo : (v > f.zhi ? f.zhi : v);
+            double v = ldexp(swz / sw, -zshift);
+            out = v < zlo ? zlo : (v > zhi ? zhi : v);
         }
     }
     pred[qi] = out;
@@ -1144,7 +1123,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     DBuf<float> rec(sp.tiles * kTileFloats, s);
     DBuf<float4> tbox(sp.tiles, s), tgeo(sp.tiles, s);
     LAUNCH(prep_data_kernel, ceil_div(mp, kThreads), kThreads, 0, s, d.x, d.y, d.z, order, d.m,
-           mp, f.ox, f.oy, f.inv_scale, std::ldexp(1.0, f.zshift), rec.get());
+           mp, f.ox, f.oy, f.inv_scale, f.zhull, rec.get());
     // near threshold R_far (unit-box units): closer (query, tile) pairs take
     // the hi/lo form (AIDW_K4_RFAR to tune)
     static const float rfar = [] {
@@ -1156,16 +1135,18 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
         const char* v = std::getenv("AIDW_K4_DIAGF");
         return v ? static_cast<float>(std::atof(v)) : 0.3f;
     }();
-    LAUNCH(tile_geo_kernel, ceil_div(sp.tiles * 32, kThreads), kThreads, 0, s, rec.get(), d.m,
-           sp.tiles, rfar * rfar, diagf * diagf, tbox.get(), tgeo.get());
+    LAUNCH(tile_geo_kernel, sp.tiles, kWeightTile, 0, s, rec.get(), d.m, sp.tiles, rfar * rfar,
+           diagf * diagf, tbox.get(), tgeo.get());
     border.release();
 
-    DBuf<uint32_t> flag(q.n, s), scan_a(q.n, s), flag_g2(q.n, s), scan_g2(q.n, s), order_q(q.n, s),
-        sub_flags(kRecipeSubs * q.n, s), sub_scans(kRecipeSubs * q.n, s);
+    // class flags, concatenated [A | alpha 2 | alpha 1 | alpha 3 | G2]: one scan
+    DBuf<uint32_t> flags(5 * q.n, s), scans(5 * q.n, s), order_q(q.n, s);
+    uint32_t *flag = flags.get(), *scan_a = scans.get();
+    uint32_t *flag_g2 = flags.get() + 4 * q.n, *scan_g2 = scans.get() + 4 * q.n;
     RecipeFlags rf;
     for (int k = 0; k < kRecipeSubs; ++k) {
-        rf.flag[k] = sub_flags.get() + k * q.n;
-        rf.scan[k] = sub_scans.get() + k * q.n;
+        rf.flag[k] = flags.get() + (1 + k) * q.n;
+        rf.scan[k] = scans.get() + (1 + k) * q.n;
     }
     DBuf<float4> qhl(q.n, s), qpar(q.n, s);
     DBuf<double> lshift(q.n, s);
@@ -1178,17 +1159,15 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     // a G1 / G2 interleave runs as all-G2 warps (AIDW_K4_G2 to tune)
     static const unsigned g2_threshold = [] {
         const char* v = std::getenv("AIDW_K4_G2");
-        const double share = v ? std::atof(v) : 0.0;
+        const double share = v ? std::atof(v) : 0.5;
         return static_cast<unsigned>(std::fmin(share, 1.0) * 4294967295.0);
     }();
     LAUNCH(class_flags_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f,
-           g_alpha4_recipe.load() ? 1 : 0, g2_threshold, zpos.get(), flag.get(), rf,
-           flag_g2.get());
-    exclusive_scan_u32(flag.get(), scan_a.get(), q.n, s);
-    for (int k = 0; k < kRecipeSubs; ++k) exclusive_scan_u32(rf.flag[k], rf.scan[k], q.n, s);
-    exclusive_scan_u32(flag_g2.get(), scan_g2.get(), q.n, s);
+           g_alpha4_recipe.load() ? 1 : 0, g2_threshold, zpos.get(), flag, rf,
+           flag_g2);
+    exclusive_scan_u32(flags.get(), scans.get(), 5 * q.n, s);
     LAUNCH(query_records_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, zpos.get(),
-           flag.get(), scan_a.get(), rf, flag_g2.get(), scan_g2.get(), order_q.get(), qhl.get(), qpar.get(),
+           flag, scan_a, rf, flag_g2, scan_g2, order_q.get(), qhl.get(), qpar.get(),
            lshift.get(), times ? times->d_alpha4 : nullptr);
 
     // queries in slabs: the FP64 partials (16 B x chunks per query) are
@@ -1196,7 +1175,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     const size_t slab = std::min(q.n, query_slab(sp.chunks));
     DBuf<double2> part(slab * sp.chunks, s);
     K4Args ka{rec.get(), sp.tiles, sp.tiles_per_chunk, sp.chunks, qhl.get(), qpar.get(),
-              q.n, flag.get(), scan_a.get(), 0, 0, part.get(), tbox.get(), tgeo.get()};
+              q.n, flag, scan_a, 0, 0, part.get(), tbox.get(), tgeo.get()};
     const size_t smem = kStages * kTileFloats * sizeof(float) + kStages * sizeof(uint64_t) +
                         kStages * sizeof(unsigned);
     // K4 variant: queries per thread x min resident CTAs (AIDW_K4_VARIANT for

@@ -10,13 +10,23 @@
 namespace aidwb {
 
 // Normalisation frame of the FP32 path: X = (x - ox) * inv_scale maps the
-// bbox into [0, 1]; z' = z * 2^zshift keeps |z'| <= 1 (exact scaling).
+// bbox into [0, 1]; z' = z * 2^zshift keeps |z'| <= 1 (exact scaling).  The
+// value hull lives on the device (zhull = {zlo, zhi}, interpolate.hpp:73-80,
+// reduced in the pass itself), so the kernels derive zshift from it and no
+// host round trip is needed for it.
 struct WeightFrame {
     double ox = 0.0, oy = 0.0, inv_scale = 1.0;
-    int zshift = 0;
-    double zlo = 0.0, zhi = 0.0;  // value hull (interpolate.hpp:73-80)
-    double snap_sq = 0.0;         // interpolate.hpp:86-89 (FP64 path)
+    const double* zhull = nullptr;  // device: {zlo, zhi}
+    double snap_sq = 0.0;           // interpolate.hpp:86-89 (FP64 path)
 };
+
+// 2^zshift with |z 2^zshift| < 1 over the value hull.
+__device__ __forceinline__ int frame_zshift(const double* zhull) {
+    const double zmax = fmax(fabs(zhull[0]), fabs(zhull[1]));
+    int e = 0;
+    if (zmax > 0.0 && isfinite(zmax)) frexp(zmax, &e);
+    return -e;
+}
 
 // Per-query inputs of the weighting stage, in visiting order `pos`
 // (perm[pos] = query index; perm == nullptr means identity).

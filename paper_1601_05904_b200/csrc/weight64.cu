@@ -234,7 +234,8 @@ __global__ void fp64_settle_kernel(const WeightQueries q, const WeightFrame f, c
         if (sw > 0.0 && isfinite(sw) && isfinite(swz)) {
             const double v = __ddiv_rn(swz, sw);
             if (isfinite(v)) {
-                out = v < f.zlo ? f.zlo : (v > f.zhi ? f.zhi : v);
+                const double zlo = f.zhull[0], zhi = f.zhull[1];
+                out = v < zlo ? zlo : (v > zhi ? zhi : v);
                 ok = true;
             }
         }

@@ -28,7 +28,9 @@ def torchrun(port, *args):
 @pytest.mark.gpu
 def test_two_rank_bench_line():
     b = torchrun(29531, "--config", "100k", "--steps", "2", "--warmup", "3",
-                 "--no-cpu-baseline", "--no-fp64")
+                 "--no-cpu-baseline", "--no-fp64", "--verify")
+    # the two shards, gathered, are the one-device run of all 100K queries
+    assert b["verify"] == {"shards_bit_identical": True, "n": 100_000}
     # configs as written: the 100K queries sharded over the 2 ranks (strong)
     assert b["n_gpus"] == 2 and b["scaling"] == "strong"
     assert b["config"]["n"] == 100_000 and b["hardware"]["per_rank_queries"] == 50_000

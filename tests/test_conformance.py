@@ -62,10 +62,15 @@ def test_reference_gpu_suites_fp32(suite):
 
 # Criteria 6-8 are host wall-clock ratios between stages / engines of the
 # SAME implementation (stage shares, grid-vs-brute kNN, grid-vs-brute
-# pipeline), written for a CPU build.  Here the GPU brute engine scans 1e10
-# FP64 candidates in ~20 ms, so host-side KnnResult materialisation is the
-# grid pipeline's largest term: 8 lands at 1.4-1.56x around its 1.5x floor.
-HOST_TIMING_CRITERIA = {6, 7, 8}
+# pipeline), written for a CPU build.  With the GridIndex device mirror, the
+# pinned result staging and the pre-built KnnResult storage, 7 (grid kNN
+# stage <= 0.2x brute; measured 0.15) and 8 (grid pipeline >= 1.5x brute;
+# 1.94x FP32, 1.65x FP64) pass in both precisions (profiles/r02/acceptance_*).
+# 6 asks the kNN share of a GPU pipeline to fall strictly from 10K to 50K to
+# 100K: it holds in FP64 (40 / 32 / 13 %); in FP32 the 10K and 50K shares
+# are within noise of each other (39 / 43 %, host-call-bound at these sizes),
+# so 6 stays a host-timing criterion.
+HOST_TIMING_CRITERIA = {6}
 
 
 def acceptance_failures(out):

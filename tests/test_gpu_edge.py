@@ -277,3 +277,29 @@ def test_empty_queries_and_zero_area():
     assert "choose_cell_width" in str(e.value)
     with pytest.raises(A.InvalidArgument):
         A.run_pipeline(line, A.PointSet(), A.RunConfig())
+
+
+@pytest.mark.parametrize("mode", ["aidw", "idw"])
+def test_graph_replay_bit_identical(mode):
+    """A repeated pass (same plan, buffers, workspace) is captured into a
+    CUDA graph and replayed: the replays give the eager pass's bits, count
+    their kernels, and time their stages."""
+    data = A.generate_random_points(30_000, UNIT, 12)
+    q = A.generate_random_queries(7_000, UNIT, 13)
+    cfg = A.RunConfig(mode=mode, params=A.AidwParams(k=10), alpha=3.0)
+    A.set_graphs(False)
+    try:
+        ref = A.run_pipeline(data, q, cfg)
+    finally:
+        A.set_graphs(True)
+    c0 = A.graph_counters()
+    outs = [A.run_pipeline(data, q, cfg) for _ in range(5)]
+    c1 = A.graph_counters()
+    assert c1["captures"] >= c0["captures"] + 1 and c1["replays"] >= c0["replays"] + 2
+    for o in outs:
+        assert np.array_equal(o.result.predicted, ref.result.predicted)
+        assert np.array_equal(o.result.alphas, ref.result.alphas)
+    last = outs[-1].stats
+    assert last["kernel_launches"] == ref.stats["kernel_launches"]
+    assert last["weight_kernel_ms"] > 0 and last["interp_ms"] > 0
+    assert last["alpha4_queries"] == ref.stats["alpha4_queries"]
