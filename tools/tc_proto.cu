@@ -32,15 +32,24 @@ using namespace aidwb::tc;
     } while (0)
 
 constexpr int kTilePts = 256;
-constexpr int kN = 128;  // MMA N (half tile)
-constexpr int kM = 128;  // queries per CTA
-constexpr int kStages = 3;
+#ifndef PROTO_N
+#define PROTO_N 128
+#endif
+#ifndef PROTO_GROUPS
+#define PROTO_GROUPS 2
+#endif
+constexpr int kN = PROTO_N;          // MMA N (tile part)
+constexpr int kParts = 256 / kN;     // MMA parts per tile
+constexpr int kM = 128;              // MMA M (queries per group)
+constexpr int kGroups = PROTO_GROUPS;  // query groups per CTA (same B operand)
+constexpr int kStages = 4;
 constexpr uint32_t kBBytes = kTilePts * kK * 4;   // 16 KB
 constexpr uint32_t kZBytes = kTilePts * 4;        // 1 KB
 constexpr uint32_t kRecBytes = kBBytes + kZBytes;
 constexpr uint32_t kABytes = kM * kK * 4;         // 8 KB
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 4 * kGroups;
 constexpr int kThreads = (kEpiWarps + 2) * 32;
+constexpr int kCtaQ = kM * kGroups;
 
 typedef unsigned long long f2;
 __device__ __forceinline__ f2 pk2(float lo, float hi) {
@@ -100,24 +109,73 @@ struct Args {
     int n, tiles;
     double2* out;
     float* dump;  // d2 of tile 0, n x 256 (or null)
+    int mode;     // 0 full, 1 TMEM loads only
 };
 
-__global__ void __launch_bounds__(kThreads, 2) far_tc_kernel(Args a) {
+#ifndef PROTO_SINGLE
+#define PROTO_SINGLE 0
+#endif
+#ifndef PROTO_C
+#define PROTO_C 32
+#endif
+constexpr int kC = PROTO_C;  // TMEM columns per load
+template <int C>
+__device__ __forceinline__ void ldc(uint32_t ta, uint32_t (&v)[C]) {
+    if constexpr (C == 128) tmem_ld128(ta, v);
+    else if constexpr (C == 64) tmem_ld64(ta, v);
+    else if constexpr (C == 32) tmem_ld32(ta, v);
+    else tmem_ld16(ta, v);
+}
+template <int C>
+__device__ __forceinline__ void ldc_after(uint32_t ta, uint32_t (&w)[C], uint32_t (&v)[C]) {
+    if constexpr (C == 32) tmem_ld32_after(ta, w, v);
+    else if constexpr (C == 16) tmem_ld16_after(ta, w, v);
+}
+// alpha = 4 far sums of C columns: w0 + w2 = (a0 + a2) rcp(a0 a2), ...
+template <int C>
+__device__ __forceinline__ void epi32(const uint32_t (&v)[C], const float* zz, f2& sw0, f2& swz0,
+                                      f2& sw1, f2& swz1) {
+#pragma unroll
+    for (int j = 0; j < C; j += 8) {
+        const float4 Za = *reinterpret_cast<const float4*>(zz + j);
+        const float4 Zb = *reinterpret_cast<const float4*>(zz + j + 4);
+        {
+            const f2 d01 = pk2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+            const f2 d23 = pk2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+            const f2 A = mul2(d01, d01), B = mul2(d23, d23);
+            const f2 rr = rcp2(mul2(A, B));
+            sw0 = fma2(rr, add2(A, B), sw0);
+            swz0 = fma2(rr, fma2(B, pk2(Za.x, Za.y), mul2(A, pk2(Za.z, Za.w))), swz0);
+        }
+        {
+            const f2 d01 = pk2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
+            const f2 d23 = pk2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
+            const f2 A = mul2(d01, d01), B = mul2(d23, d23);
+            const f2 rr = rcp2(mul2(A, B));
+            sw1 = fma2(rr, add2(A, B), sw1);
+            swz1 = fma2(rr, fma2(B, pk2(Zb.x, Zb.y), mul2(A, pk2(Zb.z, Zb.w))), swz1);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) far_tc_kernel(Args a) {
     extern __shared__ __align__(1024) char smem[];
     char* stage = smem;                                   // kStages x kRecBytes
-    char* abuf = smem + kStages * kRecBytes;              // 2 x kABytes
-    uint64_t* bar = reinterpret_cast<uint64_t*>(abuf + 2 * kABytes);
-    uint64_t *bfull = bar, *bempty = bar + kStages, *afull = bar + 2 * kStages,
-             *tfull = afull + 2, *tempty = tfull + 2;
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+    char* abuf = smem + kStages * kRecBytes;              // [group][2] x kABytes
+    uint64_t* bar = reinterpret_cast<uint64_t*>(abuf + 2 * kGroups * kABytes);
+    uint64_t *bfull = bar, *bempty = bar + kStages;
+    uint64_t* afull = bar + 2 * kStages;                  // [group][2]
+    uint64_t* tfull = afull + 2 * kGroups;                // [group][half]
+    uint64_t* tempty = tfull + 2 * kGroups;               // [group][half]
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2 * kGroups);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == kEpiWarps + 1) tmem_alloc<256>(s_tmem);
+    if (warp == kEpiWarps + 1) tmem_alloc<512>(s_tmem);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&bfull[s], 1), mbar_init(&bempty[s], 1 + kEpiWarps);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&afull[i], kEpiWarps);
+        for (int i = 0; i < 2 * kGroups; ++i) {
+            mbar_init(&afull[i], 4);
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], kEpiWarps);
+            mbar_init(&tempty[i], 4);
         }
         fence_mbar_init();
     }
@@ -142,81 +200,102 @@ __global__ void __launch_bounds__(kThreads, 2) far_tc_kernel(Args a) {
             constexpr uint32_t idesc = idesc_tf32(kM, kN);
             for (int t = 0; t < T; ++t) {
                 const int s = t % kStages;
-                mbar_wait(&afull[t & 1], (t >> 1) & 1);
                 mbar_wait(&bfull[s], (t / kStages) & 1);
+                for (int g = 0; g < kGroups; ++g) mbar_wait(&afull[g * 2 + (t & 1)], (t >> 1) & 1);
                 tc_fence_after();
-                const uint32_t a0 = smem_u32(abuf + (t & 1) * kABytes);
                 const uint32_t b0 = smem_u32(stage + s * kRecBytes);
-                for (int h = 0; h < 2; ++h) {
-                    if (t > 0) mbar_wait(&tempty[h], (t - 1) & 1);
-                    tc_fence_after();
-                    const uint32_t d = tbase + h * kN;
+                for (int h = 0; h < kParts; ++h) {
                     const uint32_t bh = b0 + h * (kN / 8) * kRowGroupBytes;
-                    mma_tf32(d, smem_desc(a0, kKChunkBytes, kRowGroupBytes),
-                             smem_desc(bh, kKChunkBytes, kRowGroupBytes), idesc, false);
-                    mma_tf32(d, smem_desc(a0 + 2 * kKChunkBytes, kKChunkBytes, kRowGroupBytes),
-                             smem_desc(bh + 2 * kKChunkBytes, kKChunkBytes, kRowGroupBytes), idesc, true);
-                    mma_commit(&tfull[h]);
+                    const int u = t * kParts + h, b = u & 1;
+                    for (int g = 0; g < kGroups; ++g) {
+                        if (u >= 2) mbar_wait(&tempty[g * 2 + b], ((u >> 1) - 1) & 1);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(abuf + (g * 2 + (t & 1)) * kABytes);
+                        const uint32_t d = tbase + (g * 2 + b) * kN;
+                        mma_tf32(d, smem_desc(a0, kKChunkBytes, kRowGroupBytes),
+                                 smem_desc(bh, kKChunkBytes, kRowGroupBytes), idesc, false);
+                        mma_tf32(d, smem_desc(a0 + 2 * kKChunkBytes, kKChunkBytes, kRowGroupBytes),
+                                 smem_desc(bh + 2 * kKChunkBytes, kKChunkBytes, kRowGroupBytes), idesc,
+                                 true);
+                        mma_commit(&tfull[g * 2 + b]);
+                    }
                 }
                 mma_commit(&bempty[s]);
             }
         }
     } else {  // ---- epilogue: one query per thread (TMEM lane)
-        const int r = warp * 32 + lane;
-        const int qi = blockIdx.x * kM + r;
+        const int g = warp >> 2, quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const int qi = blockIdx.x * kCtaQ + g * kM + r;
         const float4 q = qi < a.n ? a.qhl[qi] : make_float4(0.f, 0.f, 0.f, 0.f);
+        char* myabuf = abuf + g * 2 * kABytes;
         for (int t = 0; t < 2 && t < T; ++t) {
-            build_a(abuf + t * kABytes, r, q, a.cgeo[t]);
+            build_a(myabuf + t * kABytes, r, q, a.cgeo[t]);
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&afull[t]);
+            if (lane == 0) mbar_arrive(&afull[g * 2 + t]);
         }
         double SW = 0.0, SWZ = 0.0;
         for (int t = 0; t < T; ++t) {
             const int s = t % kStages;
             const float* z = reinterpret_cast<const float*>(stage + s * kRecBytes + kBBytes);
             f2 sw0 = 0ull, swz0 = 0ull, sw1 = 0ull, swz1 = 0ull;
-            for (int h = 0; h < 2; ++h) {
-                mbar_wait(&tfull[h], t & 1);
+            for (int h = 0; h < kParts; ++h) {
+                const int u = t * kParts + h, b = u & 1;
+                mbar_wait(&tfull[g * 2 + b], (u >> 1) & 1);
                 tc_fence_after();
-                const uint32_t ta = tbase + (static_cast<uint32_t>(warp * 32) << 16) + h * kN;
-#pragma unroll 1
-                for (int c = 0; c < kN / 32; ++c) {
-                    uint32_t v[32];
-                    tmem_ld32(ta + c * 32, v);
+                const uint32_t ta =
+                    tbase + (static_cast<uint32_t>(quarter * 32) << 16) + (g * 2 + b) * kN;
+                const float* zh = z + h * kN;
+#if PROTO_SINGLE
+                {
+                    uint32_t v[kN];
+                    ldc<kN>(ta, v);
                     tmem_wait_ld();
                     tmem_hold(v);
-                    const float* zz = z + h * kN + c * 32;
-                    if (a.dump && t == 0 && qi < a.n) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[g * 2 + b]);
+                    epi32<kN>(v, zh, sw0, swz0, sw1, swz1);
+                }
+                continue;
+#endif
+                uint32_t v[kC], w[kC];
+                ldc<kC>(ta, v);
+                tmem_wait_ld();
+                tmem_hold(v);
+                if (a.dump && t == 0 && qi < a.n) {
+                    for (int c = 0; c < kN / 32; ++c) {
+                        uint32_t uu[32];
+                        tmem_ld32(ta + 32 * c, uu);
+                        tmem_wait_ld();
+                        tmem_hold(uu);
                         for (int j = 0; j < 32; ++j)
                             a.dump[static_cast<size_t>(qi) * kTilePts + h * kN + c * 32 + j] =
-                                __uint_as_float(v[j]);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        const float4 Za = *reinterpret_cast<const float4*>(zz + j);
-                        const float4 Zb = *reinterpret_cast<const float4*>(zz + j + 4);
-                        {
-                            const f2 d01 = pk2(__uint_as_float(v[j]), __uint_as_float(v[j + 1]));
-                            const f2 d23 = pk2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-                            const f2 A = mul2(d01, d01), B = mul2(d23, d23);
-                            const f2 rr = rcp2(mul2(A, B));
-                            sw0 = fma2(rr, add2(A, B), sw0);
-                            swz0 = fma2(rr, fma2(B, pk2(Za.x, Za.y), mul2(A, pk2(Za.z, Za.w))), swz0);
-                        }
-                        {
-                            const f2 d01 = pk2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
-                            const f2 d23 = pk2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
-                            const f2 A = mul2(d01, d01), B = mul2(d23, d23);
-                            const f2 rr = rcp2(mul2(A, B));
-                            sw1 = fma2(rr, add2(A, B), sw1);
-                            swz1 = fma2(rr, fma2(B, pk2(Zb.x, Zb.y), mul2(A, pk2(Zb.z, Zb.w))), swz1);
-                        }
+                                __uint_as_float(uu[j]);
                     }
                 }
+                // kC-column chunks, the next load in flight during each chunk's sums
+#pragma unroll
+                for (int c = 0; c + 2 < kN / kC; c += 2) {
+                    ldc_after<kC>(ta + kC * (c + 1), w, v);
+                    epi32<kC>(v, zh + kC * c, sw0, swz0, sw1, swz1);
+                    tmem_wait_ld_after(sw0, swz0, sw1, swz1);
+                    tmem_hold(w);
+                    ldc_after<kC>(ta + kC * (c + 2), v, w);
+                    epi32<kC>(w, zh + kC * (c + 1), sw0, swz0, sw1, swz1);
+                    tmem_wait_ld_after(sw0, swz0, sw1, swz1);
+                    tmem_hold(v);
+                }
+                ldc_after<kC>(ta + kN - kC, w, v);
+                epi32<kC>(v, zh + kN - 2 * kC, sw0, swz0, sw1, swz1);
+                tmem_wait_ld_after(sw0, swz0, sw1, swz1);
+                tmem_hold(w);
+                // TMEM reads of this part are complete: release it to the MMA
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[h]);
+                if (lane == 0) mbar_arrive(&tempty[g * 2 + b]);
+                epi32<kC>(w, zh + kN - kC, sw0, swz0, sw1, swz1);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&bempty[s]);
@@ -226,10 +305,10 @@ __global__ void __launch_bounds__(kThreads, 2) far_tc_kernel(Args a) {
             SW += static_cast<double>(a0) + a1;
             SWZ += static_cast<double>(b0) + b1;
             if (t + 2 < T) {
-                build_a(abuf + (t & 1) * kABytes, r, q, a.cgeo[t + 2]);
+                build_a(myabuf + (t & 1) * kABytes, r, q, a.cgeo[t + 2]);
                 fence_proxy_async();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&afull[t & 1]);
+                if (lane == 0) mbar_arrive(&afull[g * 2 + (t & 1)]);
             }
         }
         if (qi < a.n) a.out[qi] = make_double2(SW, SWZ);
@@ -238,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 2) far_tc_kernel(Args a) {
     __syncthreads();
     if (warp == kEpiWarps + 1) {
         tc_fence_after();
-        tmem_dealloc<256>(tbase);
+        tmem_dealloc<512>(tbase);
     }
 }
 
@@ -310,10 +389,10 @@ int main(int argc, char** argv) {
     CKP(cudaMemcpy(d_rec, rec.data(), rec.size(), cudaMemcpyHostToDevice));
     CKP(cudaMemcpy(d_c, cgeo.data(), T * sizeof(float2), cudaMemcpyHostToDevice));
     CKP(cudaMemcpy(d_q, qhl.data(), n * sizeof(float4), cudaMemcpyHostToDevice));
-    const size_t smem = kStages * kRecBytes + 2 * kABytes + 16 * 8 + 16;
+    const size_t smem = kStages * kRecBytes + 2 * kGroups * kABytes + 32 * 8 + 16;
     CKP(cudaFuncSetAttribute(far_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const int ctas = (n + kM - 1) / kM;
-    Args args{d_rec, d_c, d_q, n, T, d_out, d_dump};
+    const int ctas = (n + kCtaQ - 1) / kCtaQ;
+    Args args{d_rec, d_c, d_q, n, T, d_out, d_dump, 0};
     far_tc_kernel<<<ctas, kThreads, smem>>>(args);
     CKP(cudaGetLastError());
     CKP(cudaDeviceSynchronize());
@@ -365,6 +444,8 @@ int main(int argc, char** argv) {
         printf("prediction (64 queries, all pairs far form): max abs err %.3e\n", emax);
     }
     args.dump = nullptr;
+    for (int mode = 0; mode < 1; ++mode) {
+    args.mode = mode;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0), cudaEventCreate(&e1);
     far_tc_kernel<<<ctas, kThreads, smem>>>(args);
@@ -378,8 +459,9 @@ int main(int argc, char** argv) {
     ms /= reps;
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    const double pairs = static_cast<double>(ctas) * kM * T * kTilePts;
-    printf("n %d tiles %d: %.3f ms, %.1f Gpair/s, %.2f pairs/SM-clk at %d MHz\n", n, T, ms,
+    const double pairs = static_cast<double>(ctas) * kCtaQ * T * kTilePts;
+    printf("mode %d n %d tiles %d: %.3f ms, %.1f Gpair/s, %.2f pairs/SM-clk at %d MHz\n", mode, n, T, ms,
            pairs / ms * 1e-6, pairs / (ms * 1e-3) / (148.0 * clk * 1e3), clk / 1000);
+    }
     return 0;
 }
