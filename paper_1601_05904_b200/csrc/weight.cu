@@ -39,13 +39,17 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdint>
+#include <string>
 
 #include "common.cuh"
 #include "weight.cuh"
+#include "weight_ops.cuh"
 
 namespace aidwb {
 
 namespace {
+
+using namespace wops;
 
 #ifndef AIDW_K4_THREADS
 #define AIDW_K4_THREADS 256
@@ -69,7 +73,6 @@ constexpr int kFarUnroll = AIDW_K4_FAR_UNROLL;  // 4-point groups per far-loop t
 #endif
 constexpr int kStages = AIDW_K4_STAGES;
 constexpr int kMaxChunks = 32;
-constexpr int kTileFloats = 9 * kWeightTile;  // SoA tile, 9 components (see kComps)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -109,35 +112,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-__device__ __forceinline__ float mufu_lg2(float x) {
-    float r;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ float mufu_ex2(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ float mufu_rcp(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
 // ------------------------------------------------------------ record prep
 __device__ __forceinline__ void split_hilo(double v, float& hi, float& lo) {
     hi = __double2float_rn(v);
     lo = __double2float_rn(v - static_cast<double>(hi));
 }
-
-// SoA components of a 256-record data tile:
-//   near form  x_hi y_hi x_lo y_lo z_hi z_lo   (unit-box coordinates, hi/lo)
-//   far form   px2 = -2 p'x, py2 = -2 p'y, pp = |p'|^2 with p' = p - c, c the
-//              tile's centre — d2 = |q'|^2 + px2 q'x + py2 q'y + pp in 3 FP32
-//              ops per pair; z_hi is shared with the near form
-enum : int { kXH, kYH, kXL, kYL, kZH, kZL, kPX, kPY, kPP, kComps };
-static_assert(kComps * kWeightTile == kTileFloats, "tile layout");
 
 // Record i = data point order[i] (8 x 8-cell blocks of the factor-4 grid, so
 // a 256-point tile is a compact square), or point i without order.
@@ -287,7 +266,6 @@ __global__ void morton_keys_kernel(const WeightQueries q, WeightFrame f, uint32_
 // Recipe sub-classes after alpha = 4 (region order): alpha = 2, 1, 3, and
 // the class codes the records carry (qpar.x and .w; general classes: 0, 2).
 constexpr int kRecipeSubs = 3;
-constexpr float kCodeA4 = 1.0f, kCodeA2 = 3.0f, kCodeA1 = 4.0f, kCodeA3 = 5.0f;
 struct RecipeFlags {
     uint32_t* flag[kRecipeSubs];
     uint32_t* scan[kRecipeSubs];
@@ -420,57 +398,8 @@ struct K4Args {
     double2* part;            // chunks x (s1 - s0) (chunk-major: coalesced), by position - s0
     const float4* tile_box;   // hi-coordinate box of every tile's real records
     const float4* tile_geo;   // {cx, cy, near threshold^2, 0}
+    unsigned classes;         // 1: general region, 2: recipe region, 3: both
 };
-
-// ---- packed f32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2): two queries per
-// 64-bit register pair; each lane rounds exactly like the scalar op, so a
-// query's result does not depend on which lane / pair it occupies.
-typedef unsigned long long f2;
-__device__ __forceinline__ f2 pk2(float lo, float hi) {
-    f2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-    return r;
-}
-__device__ __forceinline__ f2 bc2(float v) { return pk2(v, v); }
-__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
-    f2 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b) {
-    f2 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-    f2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-    f2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-__device__ __forceinline__ f2 rcp2(f2 v) {
-    float lo, hi;
-    up2(v, lo, hi);
-    return pk2(mufu_rcp(lo), mufu_rcp(hi));
-}
-
-__device__ __forceinline__ float mufu_rsq(float x) {
-    float r;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ f2 rsq2(f2 v) {
-    float lo, hi;
-    up2(v, lo, hi);
-    return pk2(mufu_rsq(lo), mufu_rsq(hi));
-}
 
 // Recipe classes (qpar.x / qpar.w code): 1 alpha = 4 (w = 1/t^2, paired
 // reciprocals), 3 alpha = 2 (w = 1/t, paired), 4 alpha = 1 (w = rsqrt t),
@@ -485,7 +414,6 @@ __device__ __forceinline__ f2 recipe_a(f2 t, f2 code) {  // paired classes: t^2 
     up2(code, c0, c1);
     return pk2(c0 == kCodeA4 ? __fmul_rn(t0, t0) : t0, c1 == kCodeA4 ? __fmul_rn(t1, t1) : t1);
 }
-__device__ __forceinline__ f2 cube2(f2 r) { return mul2(mul2(r, r), r); }
 __device__ __forceinline__ f2 recipe_rsq(f2 t, f2 code) {  // rsqrt classes: r or r^3
     const f2 r = rsq2(t);
     const f2 r3 = cube2(r);
@@ -501,50 +429,6 @@ __device__ __forceinline__ f2 sel_paired(f2 code, f2 x, f2 y) {
     up2(y, y0, y1);
     up2(code, c0, c1);
     return pk2(paired_code(c0) ? x0 : y0, paired_code(c1) ? x1 : y1);
-}
-
-// exp2 on the FMA pipe for class-G2 queries (x <= ~0 after ratio scaling):
-// Cody-Waite split x = n + f, n = rint(x) via the 1.5 * 2^23 magic add,
-// f in [-0.5, 0.5], 2^f by a degree-5 near-minimax fit (max rel. error
-// 1.9e-7 incl. FP32 Horner rounding, on par with MUFU.EX2; the degree-6 fit
-// (9.7e-8) cost 2.5 % of the general path for no measurable accuracy),
-// 2^n added into the exponent.
-// Arguments clamp at -125 (results < 2^-125 are ~0 relative to the leading
-// weight, which is 1).  Scalar and packed forms round identically.
-constexpr float kExpMagic = 12582912.0f;  // 1.5 * 2^23
-constexpr float kE0 = 1.0f, kD1 = 0.6931470036506653f, kD2 = 0.24022242426872253f,
-                kD3 = 0.05550733581185341f, kD4 = 0.009671512991189957f,
-                kD5 = 0.001326472731307149f;
-
-__device__ __forceinline__ float exp2_fma(float x) {
-    x = fmaxf(x, -125.0f);
-    const float t = x + kExpMagic;
-    const float f = x - (t - kExpMagic);
-    float p = fmaf(kD5, f, kD4);
-    p = fmaf(p, f, kD3);
-    p = fmaf(p, f, kD2);
-    p = fmaf(p, f, kD1);
-    p = fmaf(p, f, kE0);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
-__device__ __forceinline__ f2 exp2_fma2(f2 x) {
-    float lo, hi;
-    up2(x, lo, hi);
-    const f2 xc = pk2(fmaxf(lo, -125.0f), fmaxf(hi, -125.0f));
-    const f2 m = bc2(kExpMagic);
-    const f2 t = add2(xc, m);
-    const f2 f = sub2(xc, sub2(t, m));
-    f2 p = fma2(bc2(kD5), f, bc2(kD4));
-    p = fma2(p, f, bc2(kD3));
-    p = fma2(p, f, bc2(kD2));
-    p = fma2(p, f, bc2(kD1));
-    p = fma2(p, f, bc2(kE0));
-    float plo, phi, tlo, thi;
-    up2(p, plo, phi);
-    up2(t, tlo, thi);
-    return pk2(__int_as_float(__float_as_int(plo) + (__float_as_int(tlo) << 23)),
-               __int_as_float(__float_as_int(phi) + (__float_as_int(thi) << 23)));
 }
 
 // Per-thread query state: QT queries as QT/2 f32x2 pairs.
@@ -1005,6 +889,7 @@ __global__ void __launch_bounds__(kK4Threads, kMinBlocks) weight_fp32_kernel(K4A
     const size_t ctas_g = g1 > g0 ? (g1 - g0 + kQ - 1) / kQ : 0;
     const size_t b = blockIdx.x;
     if (b >= ctas_g && (r1 <= r0 || (b - ctas_g) * kQ >= r1 - r0)) return;
+    if (!(a.classes & (b < ctas_g ? 1u : 2u))) return;  // that region runs on the other engine
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&bar[s], 1);
@@ -1107,6 +992,47 @@ WeightSplit weight_split(size_t m) {
     return w;
 }
 
+bool weight_tc_selected(const WeightSplit& sp) {
+    static const int forced = [] {  // AIDW_K4_ENGINE: tuning / A-B only
+        const char* v = std::getenv("AIDW_K4_ENGINE");
+        if (!v) return -1;
+        return std::string(v) == "tc" ? 1 : std::string(v) == "simt" ? 0 : -1;
+    }();
+    if (forced >= 0) return forced == 1;
+    // enough tiles per CTA to amortise its TMEM / pipeline setup
+    return sp.tiles_per_chunk >= 4;
+}
+
+// A second stream (and fork / join events) per host thread and device for
+// the general-alpha K4 launch that runs beside the tensor-core launch.
+struct SideStream {
+    int device = -1;
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream() {
+    static thread_local SideStream cache[16];
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 16) return nullptr;
+    SideStream& c = cache[dev];
+    if (!c.s) {
+        CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming));
+        c.device = dev;
+    }
+    return &c;
+}
+
+bool weight_tc_general() {  // AIDW_TC_GENERAL=1: general-alpha queries on the TC engine too (A/B)
+    static const bool v = [] {
+        const char* e = std::getenv("AIDW_TC_GENERAL");
+        return e && std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFrame& f,
                     double* d_pred, double* d_alpha, WeightTimes* times, cudaStream_t s) {
     if (q.n == 0) return;
@@ -1138,6 +1064,12 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     LAUNCH(tile_geo_kernel, sp.tiles, kWeightTile, 0, s, rec.get(), d.m, sp.tiles, rfar * rfar,
            diagf * diagf, tbox.get(), tgeo.get());
     border.release();
+    const bool tc = weight_tc_selected(sp);
+    DBuf<char> tcrec;
+    if (tc) {
+        tcrec.alloc(weight_tc_record_bytes(sp.tiles), s);
+        weight_tc_records(rec.get(), tgeo.get(), sp.tiles, d.m, tcrec.get(), s);
+    }
 
     // class flags, concatenated [A | alpha 2 | alpha 1 | alpha 3 | G2]: one scan
     DBuf<uint32_t> flags(5 * q.n, s), scans(5 * q.n, s), order_q(q.n, s);
@@ -1175,7 +1107,7 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     const size_t slab = std::min(q.n, query_slab(sp.chunks));
     DBuf<double2> part(slab * sp.chunks, s);
     K4Args ka{rec.get(), sp.tiles, sp.tiles_per_chunk, sp.chunks, qhl.get(), qpar.get(),
-              q.n, flag, scan_a, 0, 0, part.get(), tbox.get(), tgeo.get()};
+              q.n, flag, scan_a, 0, 0, part.get(), tbox.get(), tgeo.get(), 3u};
     const size_t smem = kStages * kTileFloats * sizeof(float) + kStages * sizeof(uint64_t) +
                         kStages * sizeof(unsigned);
     // K4 variant: queries per thread x min resident CTAs (AIDW_K4_VARIANT for
@@ -1185,12 +1117,13 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
         const char* v = std::getenv("AIDW_K4_VARIANT");
         return v ? std::atoi(v) : 0;
     }();
-    auto launch = [&](auto kernel, int qt) {
+    auto launch_on = [&](auto kernel, int qt, cudaStream_t st) {
         CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
         dim3 grid(ceil_div(ka.s1 - ka.s0, static_cast<size_t>(kK4Threads) * qt) + 1, sp.chunks);
-        LAUNCH(kernel, grid, kK4Threads, smem, s, ka);
+        LAUNCH(kernel, grid, kK4Threads, smem, st, ka);
     };
+    auto launch = [&](auto kernel, int qt) { launch_on(kernel, qt, s); };
     // Few queries for the data size (n / 1024 x chunks CTAs short of ~16
     // waves of 148 x 2): 2 queries per thread, 4 CTAs / SM — twice the CTAs
     // (e.g. 20K queries x 20M points: 369 -> 215 ms).  The per-query
@@ -1203,7 +1136,36 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     for (size_t s0 = 0; s0 < q.n; s0 += slab) {
         ka.s0 = s0;
         ka.s1 = std::min(q.n, s0 + slab);
-        switch (shape) {
+        if (tc) {
+            // recipe queries on the tensor-core engine; general-alpha queries
+            // (MUFU-bound exp2 / log2, no gain from a free d2) stay on the
+            // CUDA-core kernel — the engine is a function of the query's
+            // class and of m, never of n or the shard
+            const bool gen_tc = weight_tc_general();
+            SideStream* side = gen_tc ? nullptr : side_stream();
+            if (side) {
+                // the general region on a side stream, concurrent with the TC
+                // launch (each fills the other's tail), joined before settle
+                CK(cudaEventRecord(side->fork, s));  // (a capture dependency when capturing)
+                CK(cudaStreamWaitEvent(side->s, side->fork, 0));
+                ka.classes = 1u;
+                switch (shape) {
+                    case 2: launch_on(weight_fp32_kernel<2, 4>, 2, side->s); break;
+                    default: launch_on(weight_fp32_kernel<4, AIDW_K4_MINB>, 4, side->s); break;
+                }
+                CK(cudaEventRecord(side->join, side->s));
+            }
+            WeightTcLaunch l;
+            l.tc_rec = tcrec.get();
+            l.tiles = sp.tiles, l.tiles_per_chunk = sp.tiles_per_chunk, l.chunks = sp.chunks;
+            l.qhl = qhl.get(), l.qpar = qpar.get(), l.n = q.n;
+            l.flag_a = flag, l.scan_a = scan_a;
+            l.s0 = ka.s0, l.s1 = ka.s1, l.part = part.get();
+            l.tile_box = tbox.get(), l.tile_geo = tgeo.get();
+            l.classes = gen_tc ? 3u : 2u;
+            weight_tc_launch(l, s);
+            if (side) CK(cudaStreamWaitEvent(s, side->join, 0));
+        } else switch (shape) {
             case 1: launch(weight_fp32_kernel<4, 3>, 4); break;
             case 2: launch(weight_fp32_kernel<2, 4>, 2); break;
             case 3: launch(weight_fp32_kernel<4, AIDW_K4_MINB>, 4); break;

@@ -88,6 +88,31 @@ struct WeightSplit {
 WeightSplit weight_split(size_t m);
 constexpr int kWeightTile = 256;
 
+// K4 on the tensor cores (weight_tc.cu): the far-form d2 of every (query,
+// point) pair by tcgen05 MMA.  The engine is chosen from the data split
+// alone (a function of m), so a query's result never depends on n, the
+// shard or the GPU count; AIDW_K4_ENGINE=simt / tc overrides (tuning).
+bool weight_tc_selected(const WeightSplit& sp);
+struct WeightTcLaunch {
+    const char* tc_rec = nullptr;   // weight_tc_records output
+    size_t tiles = 0, tiles_per_chunk = 0;
+    unsigned chunks = 1;
+    const float4* qhl = nullptr;
+    const float4* qpar = nullptr;
+    size_t n = 0;
+    const uint32_t* flag_a = nullptr;
+    const uint32_t* scan_a = nullptr;
+    size_t s0 = 0, s1 = 0;
+    double2* part = nullptr;
+    const float4* tile_box = nullptr;
+    const float4* tile_geo = nullptr;
+    unsigned classes = 3;  // 1: general-alpha region, 2: recipe region, 3: both
+};
+size_t weight_tc_record_bytes(size_t tiles);
+void weight_tc_records(const float* rec, const float4* tile_geo, size_t tiles, size_t m,
+                       char* tc_rec, cudaStream_t s);
+void weight_tc_launch(const WeightTcLaunch& l, cudaStream_t s);
+
 // Global switch of the alpha == 4 one-MUFU recipe (aidw_set_alpha4_recipe).
 void set_alpha4_recipe(bool enabled);
 bool alpha4_recipe_enabled();
