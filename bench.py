@@ -79,6 +79,8 @@ def peaks():
             j = json.load(f)
         p.update(hbm_gbs=float(j.get("hbm_gbs", p["hbm_gbs"])),
                  sm_max_mhz=float(j.get("sm_max_mhz", p["sm_max_mhz"])), source="measured")
+        if "bf16_tflops" in j:
+            p["bf16_tflops"] = float(j["bf16_tflops"])
     return p
 
 
@@ -517,18 +519,31 @@ def main():
     build_ms = statistics.median(s["build_ms"] for s in stats)
     build_bytes = 64 * m + 8 * (m // 4 + 1)  # factor-4 grid: ~m/4 cells (SURVEY §8 grid table)
     a4 = stats[-1]["alpha4_queries"]
+    engine = A.weight_engine(m)  # a function of m: "tensor-core" or "cuda-core"
+    tc = engine == "tensor-core"
     # Pipe roofline of the executed formula mix (K4 far-tile forms):
-    # per SM and clock the FMA pipe retires 128 FP32 ops (FFMA2 = 2) and the
-    # XU pipe 16 MUFU ops; a class is bound by the slower of the two.
-    #   recipe (alpha == 4): 3 (d2) + 1 (d2^2) + 2.5 (pair/single sums) = 6.5
-    #     FP32 + 0.75 MUFU per pair (two of every four points share one rcp)
-    #   general: G1 6 FP32 + 2 MUFU (lg2, ex2), G2 14 FP32 + 1 MUFU (ex2 as a
-    #     degree-5 polynomial); G1 / G2 split ~1:1 by coordinate hash
-    clk_recipe = max(6.5 / 128, 0.75 / 16)
+    # per SM and clock the FMA pipe retires 128 FP32 ops (FFMA2 = 2, measured
+    # profiles/r02/tmem_bench.txt) and the XU pipe 16 MUFU ops; a class is
+    # bound by the slower of the two.
+    #   recipe (alpha == 4), CUDA-core engine: 3 (d2) + 1 (d2^2) + 2.5 (pair /
+    #     single sums) = 6.5 FP32 + 0.75 MUFU per pair
+    #   recipe, tensor-core engine: d2 from the tcgen05 MMA; 1 (d2^2) + 3
+    #     (two points per reciprocal) = 4 FP32 + 0.5 MUFU per pair — both pipes
+    #     at 32 pairs / SM-clk
+    #   general (CUDA-core engine in both): G1 6 FP32 + 2 MUFU (lg2, ex2), G2
+    #     14 FP32 + 1 MUFU (ex2 as a degree-5 polynomial); G1 / G2 split ~1:1
+    ops_recipe = 4.0 if tc else 6.5
+    clk_recipe = max(4.0 / 128, 0.5 / 16) if tc else max(6.5 / 128, 0.75 / 16)
     clk_general = max(0.5 * (6 + 14) / 128, 0.5 * (2 + 1) / 16)
     clk_mix = (a4 * clk_recipe + (n - a4) * clk_general) / n
     peak_mix = sms * f_mhz * 1e6 / clk_mix / 1e9
     peak_general = sms * f_mhz * 1e6 / clk_general / 1e9
+    ops_mix = (a4 * ops_recipe + (n - a4) * 10.0) / n
+    k4_kernel = ("weight_tc_kernel (K4 recipe queries: tcgen05 kind::tf32 d2 into TMEM) + "
+                 "weight_fp32_kernel (general-alpha queries, side stream)" if tc
+                 else "weight_fp32_kernel (K4)")
+    recipe_form = ("tensor-core engine: d2 by MMA, 4 FP32 + 0.5 MUFU" if tc
+                   else "FMA-bound 6.5 FP32 + 0.75 MUFU")
 
     # general-alpha path forced (every query on exp2/log2), reported separately
     A.set_alpha4_recipe(False)
@@ -639,24 +654,32 @@ def main():
             "config": config_dict(cfg, world, scaling),
             "hardware": {"device": name, "sms": sms, "per_rank_queries": n,
                          "data_replication": "NCCL broadcast from rank 0" if world > 1 else "none"},
-            "roofline": {"bound": "fp32+mufu pipes", "kernel": "weight_fp32_kernel (K4)",
+            "roofline": {"bound": "fp32+mufu pipes", "kernel": k4_kernel, "engine": engine,
                          "achieved": achieved, "peak": peak_mix, "unit": "Gpair/s",
                          "frac": achieved / peak_mix, "traffic": k4_traffic(args.config),
                          "peak_def": f"{sms} SMs x {f_mhz:.0f} MHz ({pk['source']} sm_max_mhz) / "
                                      f"{clk_mix:.4f} SM-clk per pair: executed mix of the "
-                                     f"alpha=4 recipe ({a4} queries; FMA-bound 6.5 FP32 + "
-                                     f"0.75 MUFU) and general alpha (MUFU-bound 10 FP32 + "
-                                     f"1.5 MUFU) far-tile forms; 128 FP32 + 16 MUFU per SM-clk",
+                                     f"alpha=4 recipe ({a4} queries; {recipe_form}) and "
+                                     f"general alpha (MUFU-bound 10 FP32 + 1.5 MUFU) far-tile "
+                                     f"forms; 128 FP32 + 16 MUFU per SM-clk",
                          "frac_vs_2mufu_roofline": achieved / peak_gpairs,
                          "fp32_view": {  # the same bound as FP32 op throughput
                              "unit": "TFLOP/s (FP32 ops, FFMA = 1)",
-                             "ops_per_pair": (a4 * 6.5 + (n - a4) * 10.0) / n,
-                             "achieved": achieved * 1e9 * (a4 * 6.5 + (n - a4) * 10.0) / n / 1e12,
+                             "ops_per_pair": ops_mix,
+                             "achieved": achieved * 1e9 * ops_mix / 1e12,
                              "peak": sms * 128 * f_mhz * 1e6 / 1e12,
-                             "frac": achieved * 1e9 * (a4 * 6.5 + (n - a4) * 10.0) / n /
-                                     (sms * 128 * f_mhz * 1e6)},
+                             "frac": achieved * 1e9 * ops_mix / (sms * 128 * f_mhz * 1e6)},
                          "alpha4_recipe_queries": a4, "pairs_per_launch": pairs,
                          "k4_ms": k4_ms},
+            # the tensor-core share of K4 (recipe queries): kind::tf32 MMA,
+            # K = 16 (exact TF32 pieces) -> 32 flops per pair; dense TF32 peak
+            # taken as half the measured bf16 figure
+            "tensor_view": ({"mma": "tcgen05.mma.cta_group::1.kind::tf32 M128 N64 K16 (2 x K8)",
+                             "flops_per_pair": 32,
+                             "achieved_tflops": a4 * m * 32 / (k4_ms / 1e3) / 1e12,
+                             "peak_tflops": pk.get("bf16_tflops", 2250.0) / 2,
+                             "frac": a4 * m * 32 / (k4_ms / 1e3) / 1e12 /
+                                     (pk.get("bf16_tflops", 2250.0) / 2)} if tc else None),
             "roofline_general_alpha": {"bound": "fp32+mufu pipes (MUFU-bound)",
                                        "achieved": pairs / (k4g_ms / 1e3) / 1e9,
                                        "peak": peak_general, "unit": "Gpair/s",

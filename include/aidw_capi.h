@@ -135,6 +135,13 @@ void aidw_set_alpha4_recipe(int32_t enabled);
  * a multiple of 1024, at least 1024.  Results never depend on it. */
 void aidw_set_query_slab(int64_t queries);
 
+/* Weighting engine of the FP32 path for m data points (a function of m
+ * alone, so results never depend on n, the shard or the GPU count):
+ * 1 — recipe-class queries on the tensor-core engine (far-form d2 by tcgen05
+ * MMA, weight_tc.cu) and general-alpha queries on the CUDA-core K4 beside it;
+ * 0 — every query on the CUDA-core K4 (weight.cu; small m). */
+int32_t aidw_weight_engine(int64_t m);
+
 /* ------------------------------------------------------------ grid (K1) */
 /* build_index — grid.hpp:176-213.  sorted_ids/sorted_x/sorted_y: m entries,
  * cell_start: n_col*n_row + 1 entries (exclusive prefix). */

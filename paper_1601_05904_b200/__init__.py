@@ -13,7 +13,7 @@ from .api import (  # noqa: F401
     compute_bbox, compute_bbox_device, graph_counters, set_graphs, device_count, device_info, generate_clustered, generate_random_points,
     generate_random_queries, idw_predict_all, kernel_launch_count, knn_stage, make_grid_config,
     parse_raster_asc, raster_lattice, replication_info, raster_lattice_device, read_data_csv, read_query_csv,
-    run_pipeline, run_pipeline_device, run_raster, set_alpha4_recipe, set_devices, set_query_slab,
+    run_pipeline, run_pipeline_device, run_raster, set_alpha4_recipe, set_devices, set_query_slab, weight_engine,
     set_weight_precision,
     write_data_csv, write_query_csv, write_raster_asc, write_result_csv)
 

@@ -91,6 +91,7 @@ SIGNATURES = {
     "aidw_get_weight_precision": (C.c_int32, []),
     "aidw_set_alpha4_recipe": (None, [C.c_int32]),
     "aidw_set_query_slab": (None, [C.c_int64]),
+    "aidw_weight_engine": (C.c_int32, [C.c_int64]),
     "aidw_set_devices": (C.c_int, [_i32p, C.c_int32, _ep]),
     "aidw_device_count": (C.c_int32, []),
     "aidw_nccl_broadcast_count": (C.c_int64, []),

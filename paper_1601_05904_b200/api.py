@@ -240,6 +240,12 @@ def set_query_slab(queries: int = 0):
     lib().aidw_set_query_slab(int(queries))
 
 
+def weight_engine(m: int) -> str:
+    """FP32 weighting engine for m data points: "tensor-core" (recipe
+    queries' far-form d2 by tcgen05 MMA) or "cuda-core"."""
+    return "tensor-core" if lib().aidw_weight_engine(int(m)) else "cuda-core"
+
+
 def set_devices(ids) -> None:
     """Devices run_pipeline / run_raster spread over, one host thread each
     (query / lattice-row shards; results bit-identical to one device).

@@ -1409,6 +1409,10 @@ int32_t aidw_get_weight_precision(void) { return g_precision.load(); }
 
 void aidw_set_alpha4_recipe(int32_t enabled) { set_alpha4_recipe(enabled != 0); }
 
+int32_t aidw_weight_engine(int64_t m) {
+    return weight_tc_selected(weight_split(m > 0 ? static_cast<size_t>(m) : 0)) ? 1 : 0;
+}
+
 void aidw_set_query_slab(int64_t queries) { set_query_slab(queries > 0 ? static_cast<size_t>(queries) : 0); }
 
 int aidw_device_info(char* name, size_t cap, int32_t* sm_count, aidw_error* err) {

@@ -48,7 +48,12 @@ constexpr uint32_t kZBytes = kTilePts * 4;        // 1 KB
 constexpr uint32_t kRecBytes = kBBytes + kZBytes;
 constexpr uint32_t kABytes = kM * kK * 4;         // 8 KB
 constexpr int kEpiWarps = 4 * kGroups;
-constexpr int kThreads = (kEpiWarps + 2) * 32;
+#ifndef PROTO_CTRL
+#define PROTO_CTRL 2
+#endif
+constexpr int kCtrlWarps = PROTO_CTRL;  // 2: producer + MMA warps; 1: one warp does both
+constexpr int kThreads = (kEpiWarps + kCtrlWarps) * 32;
+constexpr int kMmaWarp = kEpiWarps + kCtrlWarps - 1;
 constexpr int kCtaQ = kM * kGroups;
 
 typedef unsigned long long f2;
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) far_tc_kernel(Args a) {
     uint64_t* tempty = tfull + 2 * kGroups;               // [group][half]
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2 * kGroups);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == kEpiWarps + 1) tmem_alloc<512>(s_tmem);
+    if (warp == kMmaWarp) tmem_alloc<512>(s_tmem);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&bfull[s], 1), mbar_init(&bempty[s], 1 + kEpiWarps);
         for (int i = 0; i < 2 * kGroups; ++i) {
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) far_tc_kernel(Args a) {
     const uint32_t tbase = *s_tmem;
     const int T = a.tiles;
 
-    if (warp == kEpiWarps) {  // ---- producer
+    if (kCtrlWarps == 2 && warp == kEpiWarps) {  // ---- producer
         if (lane == 0) {
             for (int t = 0; t < T; ++t) {
                 const int s = t % kStages;
@@ -195,9 +200,15 @@ __global__ void __launch_bounds__(kThreads, 1) far_tc_kernel(Args a) {
                           &bfull[s]);
             }
         }
-    } else if (warp == kEpiWarps + 1) {  // ---- MMA issuer
+    } else if (warp == kMmaWarp) {  // ---- MMA issuer (and producer with one control warp)
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_tf32(kM, kN);
+            if (kCtrlWarps == 1)
+                for (int t = 0; t < kStages && t < T; ++t) {
+                    mbar_expect_tx(&bfull[t], kRecBytes);
+                    bulk_load(stage + t * kRecBytes, a.rec + static_cast<size_t>(t) * kRecBytes, kRecBytes,
+                              &bfull[t]);
+                }
             for (int t = 0; t < T; ++t) {
                 const int s = t % kStages;
                 mbar_wait(&bfull[s], (t / kStages) & 1);
@@ -205,6 +216,14 @@ __global__ void __launch_bounds__(kThreads, 1) far_tc_kernel(Args a) {
                 tc_fence_after();
                 const uint32_t b0 = smem_u32(stage + s * kRecBytes);
                 for (int h = 0; h < kParts; ++h) {
+                    if (kCtrlWarps == 1 && h == kParts / 2 && t >= 1 && t - 1 + kStages < T) {
+                        // tile t - 1 consumed by every warp: refill its stage
+                        const int tp = t - 1, sp = tp % kStages;
+                        mbar_wait(&bempty[sp], (tp / kStages) & 1);
+                        mbar_expect_tx(&bfull[sp], kRecBytes);
+                        bulk_load(stage + sp * kRecBytes, a.rec + static_cast<size_t>(tp + kStages) * kRecBytes,
+                                  kRecBytes, &bfull[sp]);
+                    }
                     const uint32_t bh = b0 + h * (kN / 8) * kRowGroupBytes;
                     const int u = t * kParts + h, b = u & 1;
                     for (int g = 0; g < kGroups; ++g) {
@@ -315,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) far_tc_kernel(Args a) {
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == kEpiWarps + 1) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc<512>(tbase);
     }
