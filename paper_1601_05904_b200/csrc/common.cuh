@@ -209,6 +209,11 @@ void exclusive_scan_u32(const uint32_t* d_in, uint32_t* d_out, size_t n, cudaStr
 
 // Stable LSD radix sort of (key, value) u32 pairs on the low `bits` bits.
 void radix_sort_pairs(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaStream_t s);
+// Queries up to this count take a one-launch bucketing (top 12 key bits) for
+// the locality orders (cell order for K2, Morton order for K4) instead of
+// the radix sort: visiting order never changes a result (AIDW_SMALL_SORT_N).
+size_t small_sort_n();
+void bucket_by_key_small(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaStream_t s);
 
 // min/max reductions: out[0..3] = bbox(a ∪ b) (x,y), optional z hull out[4..5]
 void bbox_reduce_device(const double* d_ax, const double* d_ay, size_t na, const double* d_bx,

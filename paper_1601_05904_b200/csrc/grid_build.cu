@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -643,7 +644,124 @@ void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, cons
     LAUNCH(cell_ids_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_qx, d_qy, n, g,
            cells.get(), perm.get(), static_cast<uint32_t*>(nullptr), d_fail);
     const size_t total = static_cast<size_t>(g.n_col) * static_cast<size_t>(g.n_row);
-    radix_sort_pairs(cells.get(), perm.get(), n, bits_for(total - 1), s);
+    // the cell order only buys locality (every query's result is independent
+    // of the visiting order): few queries are bucketed by their key's top bits
+    // in one launch instead of the six of the two radix passes
+    if (n <= small_sort_n()) bucket_by_key_small(cells.get(), perm.get(), n, bits_for(total - 1), s);
+    else radix_sort_pairs(cells.get(), perm.get(), n, bits_for(total - 1), s);
+}
+
+// One CTA groups up to kSmallSortMax (key, value) pairs by the top B <= 12
+// bits of their `bits`-bit keys (counting sort through 2^B shared counters;
+// the order inside a bucket is unspecified — callers use it for locality
+// only).  Loads are issued kUnroll at a time: a lone CTA is latency-bound.
+constexpr int kBucketMaxBits = 12;
+constexpr int kBucketThreads = 1024;
+constexpr int kUnroll = 8;
+constexpr size_t kSmallSortMax = 65536;
+__global__ void __launch_bounds__(kBucketThreads) bucket_small_kernel(uint32_t* __restrict__ keys,
+                                                                      uint32_t* __restrict__ vals,
+                                                                      size_t n, int shift, int nb,
+                                                                      uint32_t* __restrict__ tk,
+                                                                      uint32_t* __restrict__ tv) {
+    extern __shared__ uint32_t cnt[];  // nb = 2^B counters
+    __shared__ uint32_t wsum[kBucketThreads / 32];
+    const int t = threadIdx.x;
+    for (int b = t; b < nb; b += kBucketThreads) cnt[b] = 0u;
+    __syncthreads();
+    for (size_t i0 = 0; i0 < n; i0 += static_cast<size_t>(kUnroll) * kBucketThreads) {
+        uint32_t k[kUnroll], v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const size_t i = i0 + static_cast<size_t>(u) * kBucketThreads + t;
+            k[u] = i < n ? keys[i] : 0u;
+            v[u] = i < n ? vals[i] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const size_t i = i0 + static_cast<size_t>(u) * kBucketThreads + t;
+            if (i < n) {
+                tk[i] = k[u], tv[i] = v[u];
+                atomicAdd(&cnt[k[u] >> shift], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    // exclusive scan of the counters: a contiguous run per thread, warp
+    // shuffles, then the warp totals
+    const int per = nb / kBucketThreads > 0 ? nb / kBucketThreads : 1;
+    const int b0 = t * per;
+    uint32_t run = 0;
+    for (int j = 0; j < per; ++j) run += b0 + j < nb ? cnt[b0 + j] : 0u;
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if ((t & 31) >= o) inc += x;
+    }
+    if ((t & 31) == 31) wsum[t >> 5] = inc;
+    __syncthreads();
+    if (t < 32) {
+        const uint32_t w = wsum[t];
+        uint32_t winc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, winc, o);
+            if (t >= o) winc += x;
+        }
+        wsum[t] = winc - w;
+    }
+    __syncthreads();
+    uint32_t base = wsum[t >> 5] + inc - run;
+    for (int j = 0; j < per; ++j)
+        if (b0 + j < nb) {
+            const uint32_t c = cnt[b0 + j];
+            cnt[b0 + j] = base;
+            base += c;
+        }
+    __syncthreads();
+    for (size_t i0 = 0; i0 < n; i0 += static_cast<size_t>(kUnroll) * kBucketThreads) {
+        uint32_t k[kUnroll], v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const size_t i = i0 + static_cast<size_t>(u) * kBucketThreads + t;
+            k[u] = i < n ? tk[i] : 0u;
+            v[u] = i < n ? tv[i] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const size_t i = i0 + static_cast<size_t>(u) * kBucketThreads + t;
+            if (i < n) {
+                const uint32_t pos = atomicAdd(&cnt[k[u] >> shift], 1u);
+                keys[pos] = k[u], vals[pos] = v[u];
+            }
+        }
+    }
+}
+
+void bucket_by_key_small(uint32_t* keys, uint32_t* vals, size_t n, int bits, cudaStream_t s) {
+    if (n == 0) return;
+    if (n > kSmallSortMax) {
+        radix_sort_pairs(keys, vals, n, bits, s);
+        return;
+    }
+    const int b = bits < kBucketMaxBits ? (bits > 1 ? bits : 1) : kBucketMaxBits;
+    const int shift = bits - b;
+    const int nb = 1 << b;
+    const size_t smem = static_cast<size_t>(nb) * sizeof(uint32_t);
+    CK(cudaFuncSetAttribute(bucket_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    DBuf<uint32_t> tk(n, s), tv(n, s);
+    LAUNCH(bucket_small_kernel, 1, kBucketThreads, smem, s, keys, vals, n, shift, nb, tk.get(),
+           tv.get());
+}
+
+size_t small_sort_n() {
+    static const size_t v = [] {  // AIDW_SMALL_SORT_N: tuning / A-B
+        const char* e = std::getenv("AIDW_SMALL_SORT_N");
+        return e ? static_cast<size_t>(std::atoll(e)) : static_cast<size_t>(65536);
+    }();
+    return v;
 }
 
 void bbox_reduce_device(const double* d_ax, const double* d_ay, size_t na, const double* d_bx,
@@ -653,7 +771,9 @@ void bbox_reduce_device(const double* d_ax, const double* d_ay, size_t na, const
     CK(cudaMemsetAsync(keys.get(), 0xFF, 3 * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(keys.get() + 3, 0, 3 * sizeof(unsigned long long), s));
     const size_t total = na + nb > nz ? na + nb : nz;
-    unsigned blocks = ceil_div(total ? total : 1, kThreads * 8);
+    // one value per thread while that fits 148 x 8 CTAs (a small reduction is
+    // load-latency-bound: no thread should wait on a chain of loads)
+    unsigned blocks = ceil_div(total ? total : 1, kThreads);
     if (blocks > 148u * 8u) blocks = 148u * 8u;
     LAUNCH(minmax_kernel, blocks, kThreads, 0, s, d_ax, d_ay, na, d_bx, d_by, nb, d_z, nz,
            keys.get());

@@ -920,8 +920,20 @@ __global__ void settle_kernel(const WeightQueries q, WeightFrame f, const Weight
         out = d.z[snap];
     } else {
         double sw = 0.0, swz = 0.0;
-        for (unsigned c = 0; c < chunks; ++c) {
-            const double2 v = part[static_cast<size_t>(c) * (s1 - s0) + (i - s0)];
+        const double2* pp = part + (i - s0);
+        const size_t ld = s1 - s0;
+        unsigned c = 0;
+        // eight independent loads in flight, added in chunk order (the
+        // summation order of the one-at-a-time loop)
+        for (; c + 8 <= chunks; c += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = pp[static_cast<size_t>(c + k) * ld];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sw += v[k].x, swz += v[k].y;
+        }
+        for (; c < chunks; ++c) {
+            const double2 v = pp[static_cast<size_t>(c) * ld];
             sw += v.x;
             swz += v.y;
         }
@@ -1085,7 +1097,10 @@ void weighting_fp32(const WeightQueries& q, const WeightData& d, const WeightFra
     DBuf<uint32_t> zkey(q.n, s), zpos(q.n, s);
     LAUNCH(morton_keys_kernel, ceil_div(q.n, kThreads), kThreads, 0, s, q, f, zkey.get(),
            zpos.get());
-    radix_sort_pairs(zkey.get(), zpos.get(), q.n, 16, s);
+    if (q.n <= small_sort_n())  // (visiting order only: results never depend on it)
+        bucket_by_key_small(zkey.get(), zpos.get(), q.n, 16, s);
+    else
+        radix_sort_pairs(zkey.get(), zpos.get(), q.n, 16, s);
     zkey.release();
     // share of general-alpha queries on the FMA-pipe exp2 (G2); the rest of
     // a G1 / G2 interleave runs as all-G2 warps (AIDW_K4_G2 to tune)

@@ -224,8 +224,18 @@ __global__ void fp64_settle_kernel(const WeightQueries q, const WeightFrame f, c
         out = d.z[snap];
     } else {
         double sw = 0.0, swz = 0.0;
-        for (unsigned c = 0; c < chunks; ++c) {
-            const double2 v = part[static_cast<size_t>(c) * (s1 - s0) + (slot - s0)];
+        const double2* pp = part + (slot - s0);
+        const size_t ld = s1 - s0;
+        unsigned c = 0;
+        for (; c + 8 <= chunks; c += 8) {  // loads in flight, chunk-order sums
+            double2 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = pp[static_cast<size_t>(c + k) * ld];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sw = __dadd_rn(sw, v[k].x), swz = __dadd_rn(swz, v[k].y);
+        }
+        for (; c < chunks; ++c) {
+            const double2 v = pp[static_cast<size_t>(c) * ld];
             sw = __dadd_rn(sw, v.x);
             swz = __dadd_rn(swz, v.y);
         }
