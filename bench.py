@@ -95,6 +95,20 @@ def cpu_model():
     return platform.processor() or "unknown"
 
 
+def k2_pipes(name):
+    """K2's pipe utilisation from the latest committed ncu capture (the
+    kernel is ALU / FP64-bound in its top-k network, so its HBM fraction is
+    notional; the pipes say where it stands)."""
+    import glob
+    for path in reversed(sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k2_pipes.json")))):
+        with open(path) as f:
+            j = json.load(f)
+        if j.get("config", "1m") == name:
+            return {k: j[k] for k in ("alu_pipe_pct", "fp64_pipe_pct", "issue_active_pct",
+                                      "dram_bytes_per_launch", "source") if k in j}
+    return None
+
+
 def k4_traffic(name):
     """dram__bytes_read.sum + dram__bytes_write.sum of one K4 launch from the
     latest committed `ncu --set full` capture of this config (or None)."""
@@ -694,6 +708,7 @@ def main():
                             "peak_gbs": pk["hbm_gbs"],
                             "frac": knn_bytes / (knn_ms / 1e3) / 1e9 / pk["hbm_gbs"],
                             "candidates_reference": ref_cand, "candidates_scanned": cand,
+                            "pipes_ncu": k2_pipes(args.config),
                             "note": "algorithmic bytes credit the reference's candidates; "
                                     "the kernel is ALU/FP64-bound in its top-k network "
                                     "(profiles/r02)"},

@@ -164,7 +164,18 @@ __device__ __forceinline__ double cell_lower_d2(const GridGeom& g, double fx, do
     return (dx * dx + dy * dy) * w2 * (1.0 - 1.0e-9);
 }
 
+// Points in the cell rectangle [c0, c1] x [r0, r1]: four loads of the
+// summed-area table (O(1) whatever the block size — the void queries of the
+// clustered stress case reach levels ~100), else one cell_start pair per row.
 __device__ __forceinline__ size_t rect_count(const KnnArgs& a, int c0, int c1, int r0, int r1) {
+    if (a.rect_prefix) {  // PT[c][r], column-major
+        const size_t h = static_cast<size_t>(a.g.n_row) + 1;
+        const uint32_t* P = a.rect_prefix;
+        const uint32_t* lo = P + static_cast<size_t>(c0) * h;
+        const uint32_t* hi = P + static_cast<size_t>(c1 + 1) * h;
+        // u32 arithmetic wraps exactly (every count < 2^32)
+        return __ldg(hi + r1 + 1) - __ldg(hi + r0) - __ldg(lo + r1 + 1) + __ldg(lo + r0);
+    }
     size_t total = 0;
     for (int r = r0; r <= r1; ++r) {
         const size_t base = static_cast<size_t>(r) * static_cast<size_t>(a.g.n_col);
@@ -377,14 +388,21 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
             ++level;
             const int r = level;
             const int c0 = imax(0, col - r), c1 = imin(n_col - 1, col + r);
+            const int r0 = imax(0, row - r + 1), r1 = imin(n_row - 1, row + r - 1);
+            // an empty ring (four O(1) block counts) or an empty side adds no
+            // candidate: skipping it changes nothing but the cell lookups
+            // (void queries of the stress case cross dozens of empty rings)
+            if (a.rect_prefix &&
+                rect_count(a, c0, c1, imax(0, row - r), imin(n_row - 1, row + r)) ==
+                    rect_count(a, imax(0, col - r + 1), imin(n_col - 1, col + r - 1), r0, r1))
+                continue;
             if (row - r >= 0) scan_row(a, t, qx, qy, fx, fy, inv_w2, row - r, c0, c1, snap, scanned);
             if (row + r <= n_row - 1)
                 scan_row(a, t, qx, qy, fx, fy, inv_w2, row + r, c0, c1, snap, scanned);
-            const int r0 = imax(0, row - r + 1), r1 = imin(n_row - 1, row + r - 1);
-            if (col - r >= 0)
+            if (col - r >= 0 && (!a.rect_prefix || rect_count(a, col - r, col - r, r0, r1) > 0))
                 for (int rr = r0; rr <= r1; ++rr)
                     scan_row(a, t, qx, qy, fx, fy, inv_w2, rr, col - r, col - r, snap, scanned);
-            if (col + r <= n_col - 1)
+            if (col + r <= n_col - 1 && (!a.rect_prefix || rect_count(a, col + r, col + r, r0, r1) > 0))
                 for (int rr = r0; rr <= r1; ++rr)
                     scan_row(a, t, qx, qy, fx, fy, inv_w2, rr, col + r, col + r, snap, scanned);
         }
@@ -470,8 +488,52 @@ __global__ void __launch_bounds__(128) knn_brute_kernel(KnnArgs a) {
 
 }  // namespace
 
+namespace {
+// Summed-area table of the cell counts from the CSR prefix, stored column
+// by column: PT[c][r] = points in rows < r, columns < c.  One CTA per column
+// boundary c; its threads own contiguous row ranges (sum, block scan,
+// rewrite): PT[c][r + 1] = PT[c][r] + (cell_start[r n_col + c] - cell_start[r n_col]).
+constexpr int kPrefixThreads = 256;
+__global__ void __launch_bounds__(kPrefixThreads) rect_prefix_kernel(
+    const uint32_t* __restrict__ cell_start, int n_col, int n_row, uint32_t* __restrict__ PT) {
+    __shared__ uint32_t warp_tot[kPrefixThreads / 32];
+    const int c = blockIdx.x, t = threadIdx.x;
+    const int per = (n_row + kPrefixThreads - 1) / kPrefixThreads;
+    const int r0 = t * per, r1 = r0 + per < n_row ? r0 + per : n_row;
+    auto row_count = [&](int r) {
+        const size_t base = static_cast<size_t>(r) * static_cast<size_t>(n_col);
+        return __ldg(cell_start + base + c) - __ldg(cell_start + base);
+    };
+    uint32_t sum = 0;
+    for (int r = r0; r < r1; ++r) sum += row_count(r);
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if ((t & 31) >= o) inc += v;
+    }
+    if ((t & 31) == 31) warp_tot[t >> 5] = inc;
+    __syncthreads();
+    uint32_t before = inc - sum;
+    for (int w = 0; w < (t >> 5); ++w) before += warp_tot[w];
+    uint32_t* col = PT + static_cast<size_t>(c) * (static_cast<size_t>(n_row) + 1);
+    if (t == 0) col[0] = 0;
+    for (int r = r0; r < r1; ++r) {
+        before += row_count(r);
+        col[r + 1] = before;
+    }
+}
+}  // namespace
+
 void run_knn_grid(KnnArgs a, cudaStream_t s) {
     if (a.n == 0) return;
+    DBuf<uint32_t> prefix;
+    if (!a.rect_prefix && a.m >= static_cast<size_t>(a.k)) {
+        prefix.alloc((static_cast<size_t>(a.g.n_row) + 1) * (static_cast<size_t>(a.g.n_col) + 1), s);
+        LAUNCH(rect_prefix_kernel, static_cast<unsigned>(a.g.n_col) + 1, kPrefixThreads, 0, s,
+               a.cell_start, a.g.n_col, a.g.n_row, prefix.get());
+        a.rect_prefix = prefix.get();
+    }
     DBuf<double> sd;
     DBuf<uint32_t> si;
     if (a.k_eff > 64) {

@@ -24,6 +24,10 @@ struct KnnArgs {
     const uint32_t* cell_start = nullptr;
     const uint32_t* sorted_ids = nullptr;
     const double2* sorted_xy = nullptr;  // cell-sorted {x, y}
+    // summed-area table of the cell counts, column-major (n_col + 1) x
+    // (n_row + 1): PT[c][r] = points in rows < r, columns < c (built by
+    // run_knn_grid); block counts in O(1)
+    const uint32_t* rect_prefix = nullptr;
     // data in index order — brute engine
     const double* dx = nullptr;
     const double* dy = nullptr;

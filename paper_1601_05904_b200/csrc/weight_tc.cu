@@ -53,10 +53,16 @@ using namespace tc;
 #ifndef AIDW_TC_BUFS
 #define AIDW_TC_BUFS 2
 #endif
+#ifndef AIDW_TC_SPLITLD
+#define AIDW_TC_SPLITLD 0
+#endif
 #ifndef AIDW_TC_STAGES
 #define AIDW_TC_STAGES 4
 #endif
-constexpr int kGroups = 3;                       // query groups (one MMA M = 128 each)
+#ifndef AIDW_TC_GROUPS
+#define AIDW_TC_GROUPS 3
+#endif
+constexpr int kGroups = AIDW_TC_GROUPS;          // query groups (one MMA M = 128 each)
 constexpr int kN = AIDW_TC_N;                    // MMA N: points per part
 constexpr int kParts = kWeightTile / kN;         // parts per tile
 constexpr int kBufs = AIDW_TC_BUFS;              // TMEM accumulators per group
@@ -161,11 +167,11 @@ struct QConst {
 
 // Far sums of one part (64 d2 in registers, lanes = points j, j + 1).
 // Paired classes take points (j, j + 2) and (j + 1, j + 3) on one reciprocal.
-template <int CLS>
-__device__ __forceinline__ void far_part(const uint32_t (&v)[kN], const float* __restrict__ z,
+template <int CLS, int C = kN>
+__device__ __forceinline__ void far_part(const uint32_t (&v)[C], const float* __restrict__ z,
                                          const QConst& qc, f2& sw0, f2& swz0, f2& sw1, f2& swz1) {
 #pragma unroll
-    for (int j = 0; j < kN; j += 8) {
+    for (int j = 0; j < C; j += 8) {
         const float4 Za = *reinterpret_cast<const float4*>(z + j);
         const float4 Zb = *reinterpret_cast<const float4*>(z + j + 4);
 #pragma unroll
@@ -218,16 +224,54 @@ __device__ __forceinline__ void far_part(const uint32_t (&v)[kN], const float* _
     }
 }
 
-__device__ __forceinline__ void far_part_mixed(int cls, const uint32_t (&v)[kN],
+template <int C>
+__device__ __forceinline__ void far_part_mixed(int cls, const uint32_t (&v)[C],
                                                const float* __restrict__ z, const QConst& qc,
                                                f2& sw0, f2& swz0, f2& sw1, f2& swz1) {
     switch (cls) {  // divergent, each lane its own class's form
-        case kClsA4: far_part<kClsA4>(v, z, qc, sw0, swz0, sw1, swz1); break;
-        case kClsA2: far_part<kClsA2>(v, z, qc, sw0, swz0, sw1, swz1); break;
-        case kClsA1: far_part<kClsA1>(v, z, qc, sw0, swz0, sw1, swz1); break;
-        case kClsA3: far_part<kClsA3>(v, z, qc, sw0, swz0, sw1, swz1); break;
-        default: far_part<kClsG>(v, z, qc, sw0, swz0, sw1, swz1); break;
+        case kClsA4: far_part<kClsA4, C>(v, z, qc, sw0, swz0, sw1, swz1); break;
+        case kClsA2: far_part<kClsA2, C>(v, z, qc, sw0, swz0, sw1, swz1); break;
+        case kClsA1: far_part<kClsA1, C>(v, z, qc, sw0, swz0, sw1, swz1); break;
+        case kClsA3: far_part<kClsA3, C>(v, z, qc, sw0, swz0, sw1, swz1); break;
+        default: far_part<kClsG, C>(v, z, qc, sw0, swz0, sw1, swz1); break;
     }
+}
+
+// One part's far sums from TMEM.  Default: one x64 load, released at once,
+// then the sums.  AIDW_TC_SPLITLD: two x32 loads, the second in flight
+// while the first half's sums run.
+template <int MODE>
+__device__ __forceinline__ void far_tmem_part(uint32_t ta, const float* __restrict__ z, int cls,
+                                              const QConst& qc, uint64_t* tempty, int lane,
+                                              f2& sw0, f2& swz0, f2& sw1, f2& swz1) {
+#if AIDW_TC_SPLITLD
+    static_assert(kN == 64, "split load: two 32-column halves");
+    uint32_t lo[32], hi[32];
+    tmem_ld32(ta, lo);
+    tmem_wait_ld();
+    tmem_hold(lo);
+    tmem_ld32_after(ta + 32, hi, lo);
+    if (MODE == kClsMixed) far_part_mixed<32>(cls, lo, z, qc, sw0, swz0, sw1, swz1);
+    else far_part<MODE, 32>(lo, z, qc, sw0, swz0, sw1, swz1);
+    tmem_wait_ld_after(sw0, swz0, sw1, swz1);
+    tmem_hold(hi);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty);
+    if (MODE == kClsMixed) far_part_mixed<32>(cls, hi, z + 32, qc, sw0, swz0, sw1, swz1);
+    else far_part<MODE, 32>(hi, z + 32, qc, sw0, swz0, sw1, swz1);
+#else
+    uint32_t v[kN];
+    tmem_ld(ta, v);
+    tmem_wait_ld();
+    tmem_hold(v);
+    // the registers hold the part: release the buffer to the next MMA
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty);
+    if (MODE == kClsMixed) far_part_mixed<kN>(cls, v, z, qc, sw0, swz0, sw1, swz1);
+    else far_part<MODE>(v, z, qc, sw0, swz0, sw1, swz1);
+#endif
 }
 
 // Near weight of a pair of points for one query (the hi/lo distance d2).
@@ -406,18 +450,9 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const Smem& sm, uint32
             const int u = t * kParts + h, b = u % kBufs;
             mbar_wait(&sm.tfull[g * kBufs + b], (u / kBufs) & 1);
             tc_fence_after();
-            uint32_t v[kN];
             const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + (g * kBufs + b) * kN;
-            tmem_ld(ta, v);
-            tmem_wait_ld();
-            tmem_hold(v);
-            // the registers hold the part: release the buffer to the next MMA
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.tempty[g * kBufs + b]);
-            const float* z = nf + kNZH * kWeightTile + h * kN;
-            if (MODE == kClsMixed) far_part_mixed(cls, v, z, qc, sw0, swz0, sw1, swz1);
-            else far_part<MODE>(v, z, qc, sw0, swz0, sw1, swz1);
+            far_tmem_part<MODE>(ta, nf + kNZH * kWeightTile + h * kN, cls, qc,
+                                &sm.tempty[g * kBufs + b], lane, sw0, swz0, sw1, swz1);
         }
         if (!nq) {
             float w0, w1, z0, z1;
