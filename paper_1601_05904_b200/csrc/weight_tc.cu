@@ -13,12 +13,11 @@
 // (|q'| + |p'|)^2 (measured max 1.6e-6 relative on far pairs, tools/tc_proto.cu).
 //
 // Layout: one CTA per SM, 3 query groups x 128 queries (one TMEM lane each),
-// 12 epilogue warps (a group's 4 warps cover TMEM lanes 0-127) and one
-// control warp whose lane 0 streams 22.5 KB tile records (B operand + near
-// components) into a 4-stage shared-memory ring with the bulk-copy engine
-// and issues the MMAs into two 64-column TMEM buffers per group.  (A
-// producer warp plus one MMA warp per group measured 4 % slower: 16 warps
-// instead of 13 share the issue slots.)  An
+// 12 epilogue warps (a group's 4 warps cover TMEM lanes 0-127), a producer
+// warp whose lane 0 streams 22.5 KB tile records (B operand + near
+// components) into a 4-stage shared-memory ring with the bulk-copy engine,
+// and a control warp whose lane 0 issues the MMAs into two 64-column TMEM
+// buffers per group.  An
 // epilogue thread owns one query: per 64-point part it loads its 64 d2 with
 // one tcgen05.ld (32x32b.x64), releases the buffer to the next MMA at once
 // and runs its class's weight form on the registers (alpha = 4: two points
@@ -67,9 +66,24 @@ constexpr int kN = AIDW_TC_N;                    // MMA N: points per part
 constexpr int kParts = kWeightTile / kN;         // parts per tile
 constexpr int kBufs = AIDW_TC_BUFS;              // TMEM accumulators per group
 constexpr int kStages = AIDW_TC_STAGES;          // tile records in flight
+#ifndef AIDW_TC_NONEAR_DEBUG
+#define AIDW_TC_NONEAR_DEBUG 0  // timing experiments only: skip the near passes (wrong sums)
+#endif
+#ifndef AIDW_TC_TRACE
+#define AIDW_TC_TRACE 0  // timing experiments only: per-warp wait cycles of one CTA (printf)
+#endif
+#if AIDW_TC_TRACE
+#define TRACE_T0(v) const long long v = clock64()
+#define TRACE_ADD(acc, v0) acc += clock64() - (v0)
+#define TRACE_CTA (blockIdx.x == 200 && blockIdx.y == 5)
+#else
+#define TRACE_T0(v)
+#define TRACE_ADD(acc, v0)
+#endif
 constexpr int kEpiWarps = 4 * kGroups;
-constexpr int kCtlWarp = kEpiWarps;              // TMA + MMA (lane 0), TMEM owner
-constexpr int kTcThreads = (kEpiWarps + 1) * 32;
+constexpr int kCtlWarp = kEpiWarps;              // MMA issue (lane 0), TMEM owner
+constexpr int kProdWarp = kEpiWarps + 1;         // stage refills (lane 0)
+constexpr int kTcThreads = (kEpiWarps + 2) * 32;
 constexpr int kCtaQ = 128 * kGroups;             // queries per CTA
 constexpr uint32_t kBBytes = kWeightTile * kK * 4;           // 16 KB B operand
 constexpr uint32_t kNearBytes = 6 * kWeightTile * 4;         // z and near-form coordinates
@@ -381,48 +395,77 @@ __device__ __forceinline__ Smem carve(char* smem) {
     return s;
 }
 
-// Control warp, lane 0: tile records through the stage ring (bulk-copy
-// engine) and the MMAs into TMEM.  A stage is refilled once every MMA and
-// every epilogue warp is done with its tile; the refill wait sits between
-// the halves of the next tile's parts so it never holds back an MMA that
-// could already run.
-__device__ __forceinline__ void control(const TcArgs& a, const Smem& sm, uint32_t tbase, size_t t0,
-                                        int T) {
-    constexpr uint32_t idesc = idesc_tf32(128, kN);
-    for (int t = 0; t < kStages && t < T; ++t) {
-        mbar_expect_tx(&sm.bfull[t], kRecBytes);
-        bulk_load(sm.stage + t * kRecBytes, a.rec + (t0 + t) * kRecBytes, kRecBytes, &sm.bfull[t]);
-    }
+// Producer warp, lane 0: tile records through the stage ring (bulk-copy
+// engine).  A stage is refilled once every epilogue warp and every group's
+// MMAs are done with its tile.
+__device__ __forceinline__ void producer(const TcArgs& a, const Smem& sm, size_t t0, int T) {
     for (int t = 0; t < T; ++t) {
         const int s = t % kStages;
+        if (t >= kStages) mbar_wait(&sm.bempty[s], ((t / kStages) - 1) & 1);
+        mbar_expect_tx(&sm.bfull[s], kRecBytes);
+        bulk_load(sm.stage + s * kRecBytes, a.rec + (t0 + t) * kRecBytes, kRecBytes, &sm.bfull[s]);
+    }
+}
+
+// MMA issuer, the control warp: parts in order, for each part the groups
+// in order.  Group g's part u = (tile t, part h) needs the tile's stage
+// (bfull), the group's A rows for t (afull) and its TMEM buffer u % kBufs
+// released (tempty).  After the last part of a tile the MMAs' completion
+// releases the stage (bempty counts one commit per group).  The whole warp
+// runs the loop (warp-uniform addresses and descriptors live in uniform
+// registers) and one elected lane issues: sub-partition 0 also hosts three
+// epilogue warps, and every group has a warp there, so the issuer's
+// instruction count paces the CTA.  (Measured alternatives, no gain or
+// worse: the refill wait inside this loop, one issuer warp per group on
+// sub-partitions 1-3, a non-blocking per-group issue loop — 30 % slower:
+// its polling takes issue slots from sub-partition 0's epilogue warps.)
+__device__ __forceinline__ void issuer(const Smem& sm, uint32_t tbase, int T) {
+    constexpr uint32_t idesc = idesc_tf32(128, kN);
+    const uint64_t desc0 = smem_desc(0, kKChunkBytes, kRowGroupBytes);
+    const uint32_t stage0 = smem_u32(sm.stage), abuf0 = smem_u32(sm.abuf);
+#if AIDW_TC_TRACE
+    long long wb = 0, wa = 0, we[kGroups] = {}, tall = clock64();
+#endif
+    for (int t = 0; t < T; ++t) {
+        const int s = t % kStages;
+        TRACE_T0(c0);
         mbar_wait(&sm.bfull[s], (t / kStages) & 1);
+        TRACE_ADD(wb, c0);
+        TRACE_T0(c1);
         for (int g = 0; g < kGroups; ++g) mbar_wait(&sm.afull[g * 2 + (t & 1)], (t >> 1) & 1);
+        TRACE_ADD(wa, c1);
         tc_fence_after();
-        const uint32_t b0 = smem_u32(sm.stage + s * kRecBytes);
+        const uint32_t b0 = stage0 + s * kRecBytes;
+#pragma unroll
         for (int h = 0; h < kParts; ++h) {
-            if (h == kParts / 2 && t >= 1 && t - 1 + kStages < T) {
-                const int tp = t - 1, sp = tp % kStages;
-                mbar_wait(&sm.bempty[sp], (tp / kStages) & 1);
-                mbar_expect_tx(&sm.bfull[sp], kRecBytes);
-                bulk_load(sm.stage + sp * kRecBytes, a.rec + (t0 + tp + kStages) * kRecBytes,
-                          kRecBytes, &sm.bfull[sp]);
-            }
             const uint32_t bh = b0 + h * (kN / 8) * kRowGroupBytes;
             const int u = t * kParts + h, b = u % kBufs;
+#pragma unroll
             for (int g = 0; g < kGroups; ++g) {
+                TRACE_T0(c2);
                 if (u >= kBufs) mbar_wait(&sm.tempty[g * kBufs + b], ((u / kBufs) - 1) & 1);
+                TRACE_ADD(we[g], c2);
                 tc_fence_after();
-                const uint32_t a0 = smem_u32(sm.abuf + (g * 2 + (t & 1)) * kABytes);
+                const uint32_t a0 = abuf0 + (g * 2 + (t & 1)) * kABytes;
                 const uint32_t d = tbase + (g * kBufs + b) * kN;
-                mma_tf32(d, smem_desc(a0, kKChunkBytes, kRowGroupBytes),
-                         smem_desc(bh, kKChunkBytes, kRowGroupBytes), idesc, false);
-                mma_tf32(d, smem_desc(a0 + 2 * kKChunkBytes, kKChunkBytes, kRowGroupBytes),
-                         smem_desc(bh + 2 * kKChunkBytes, kKChunkBytes, kRowGroupBytes), idesc, true);
-                mma_commit(&sm.tfull[g * kBufs + b]);
+                if (elect_one()) {
+                    mma_tf32(d, smem_desc_at(desc0, a0), smem_desc_at(desc0, bh), idesc, false);
+                    mma_tf32(d, smem_desc_at(desc0, a0 + 2 * kKChunkBytes),
+                             smem_desc_at(desc0, bh + 2 * kKChunkBytes), idesc, true);
+                    mma_commit(&sm.tfull[g * kBufs + b]);
+                }
+                __syncwarp();
             }
         }
-        mma_commit(&sm.bempty[s]);
+        if (elect_one())
+            for (int g = 0; g < kGroups; ++g) mma_commit(&sm.bempty[s]);
+        __syncwarp();
     }
+#if AIDW_TC_TRACE
+    if (TRACE_CTA && (threadIdx.x & 31) == 0)
+        printf("issuer: total %lld  wait bfull %lld afull %lld tempty g0 %lld g1 %lld g2 %lld (T %d)\n",
+               clock64() - tall, wb, wa, we[0], we[1], we[kGroups - 1], T);
+#endif
 }
 
 // Epilogue warp: the tile loop for one weight form (MODE = a class, or
@@ -434,11 +477,13 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const Smem& sm, uint32
                                          double& SW, double& SWZ) {
     const int r = quarter * 32 + lane;
     char* myabuf = sm.abuf + g * 2 * kABytes;
+#if AIDW_TC_TRACE
+    long long wf = 0, tpart = 0, ttile = 0, tall = clock64();
+#endif
     for (int t = 0; t < T; ++t) {
         const int s = t % kStages;
         const char* st = sm.stage + s * kRecBytes;
         const float* nf = reinterpret_cast<const float*>(st + kBBytes);
-        // (query, tile) near test on the hi coordinates (as weight.cu)
         const float4 tb = __ldg(a.tile_box + t0 + t);
         const float4 tg = __ldg(a.tile_geo + t0 + t);
         const float ex = fmaxf(0.0f, fmaxf(tb.x - q.x, q.x - tb.z));
@@ -448,12 +493,20 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const Smem& sm, uint32
 #pragma unroll 1
         for (int h = 0; h < kParts; ++h) {
             const int u = t * kParts + h, b = u % kBufs;
+            TRACE_T0(c0);
             mbar_wait(&sm.tfull[g * kBufs + b], (u / kBufs) & 1);
+            TRACE_ADD(wf, c0);
+            TRACE_T0(c1);
             tc_fence_after();
             const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + (g * kBufs + b) * kN;
             far_tmem_part<MODE>(ta, nf + kNZH * kWeightTile + h * kN, cls, qc,
                                 &sm.tempty[g * kBufs + b], lane, sw0, swz0, sw1, swz1);
+#if AIDW_TC_TRACE
+            tmem_hold_f2(sw0, swz0, sw1, swz1);
+#endif
+            TRACE_ADD(tpart, c1);
         }
+        TRACE_T0(c3);
         if (!nq) {
             float w0, w1, z0, z1;
             up2(add2(sw0, sw1), w0, w1);
@@ -461,7 +514,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const Smem& sm, uint32
             SW += (static_cast<double>(w0) + static_cast<double>(w1)) * m0;
             SWZ += (static_cast<double>(z0) + static_cast<double>(z1)) * m0;
         }
-        if (__any_sync(0xFFFFFFFFu, valid && nq)) {
+        if (!AIDW_TC_NONEAR_DEBUG && __any_sync(0xFFFFFFFFu, valid && nq)) {
             double nw = 0.0, nz = 0.0;
             if (MODE == kClsMixed) near_tile_any(cls, nf, q, qc, nw, nz);
             else near_tile<MODE>(nf, q, qc, nw, nz);
@@ -475,7 +528,13 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const Smem& sm, uint32
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.afull[g * 2 + (t & 1)]);
         }
+        TRACE_ADD(ttile, c3);
     }
+#if AIDW_TC_TRACE
+    if (TRACE_CTA && lane == 0)
+        printf("epi g%d q%d: total %lld  wait tfull %lld  parts %lld  tile tail %lld\n", g, quarter,
+               clock64() - tall, wf, tpart, ttile);
+#endif
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) weight_tc_kernel(TcArgs a) {
@@ -513,7 +572,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) weight_tc_kernel(TcArgs a) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.bfull[s], 1);
-            mbar_init(&sm.bempty[s], 1 + kEpiWarps);
+            mbar_init(&sm.bempty[s], kGroups + kEpiWarps);
         }
         for (int i = 0; i < 2 * kGroups; ++i) mbar_init(&sm.afull[i], 4);
         for (int i = 0; i < kBufs * kGroups; ++i) {
@@ -528,7 +587,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) weight_tc_kernel(TcArgs a) {
     const uint32_t tbase = *sm.tmem_slot;
 
     if (warp == kCtlWarp) {
-        if (lane == 0) control(a, sm, tbase, t0, T);
+        issuer(sm, tbase, T);
+    } else if (warp == kProdWarp) {
+        if (lane == 0) producer(a, sm, t0, T);
     } else {
         float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
         float4 par = make_float4(recipe ? kCodeA4 : -1.0f, 0.f, 1.f, recipe ? kCodeA4 : 0.f);
