@@ -15,10 +15,14 @@
 // requires, so dist_sq keeps its two-products-then-add rounding.
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstddef>
 #include <condition_variable>
 #include <cstdint>
+#include <iterator>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -188,14 +192,28 @@ inline KnnResult grid_knn(const QueryPoint& q, const GridIndex& index, int k) {
 
 namespace detail {
 
-/// Host-side result storage of knn_stage: n KnnResult objects whose
+inline double ms_since(std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+}
+/// AIDW_HOST_TRACE=1: per-call phase times of the host side on stderr.
+inline bool host_trace() {
+    static const bool on = [] {
+        const char* v = std::getenv("AIDW_HOST_TRACE");
+        return v && *v == '1';
+    }();
+    return on;
+}
+
+/// Host-side result storage of knn_stage: KnnResult objects whose
 /// distances_sq vectors already hold k elements.  Building them is pure host
-/// work dominated by first-touch page faults of the fresh heap (~2-3 ms per
-/// 100K results), so a background thread builds the next call's storage
-/// after each call — sized by the largest request seen, doubled (like a
-/// vector's capacity), capped at 64 MiB — and a call with a matching k takes
-/// it with no allocation.  Otherwise the storage is built on the host pool
-/// while the device runs the stage.
+/// work — one heap allocation per result plus first-touch page faults
+/// (~3 ms per 100K results on one thread) — so after each call a background
+/// thread tops the stash up to 4x the largest request seen (capped at
+/// 64 MiB) in batches that are usable as soon as they land; a call with a
+/// matching k moves its n results out of the stash's tail (the rest stays
+/// for the next call: no frees on the call path) and builds whatever is
+/// missing on the host pool while the device runs the stage (the top-up
+/// pauses meanwhile).
 class ResultStash {
 public:
     static ResultStash& instance() {
@@ -203,34 +221,41 @@ public:
         return stash;
     }
 
-    /// n results with distances_sq.size() == k.
+    /// n results with distances_sq.size() == k: the stash's tail, and what
+    /// it lacks built on the host pool (the background top-up pauses).
     std::vector<KnnResult> take(std::size_t n, std::size_t k) {
+        std::vector<KnnResult> v;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            if (ready_ && k_ == k && stash_.size() >= n) {
-                std::vector<KnnResult> v = std::move(stash_);
-                stash_.clear();
-                ready_ = false;
-                v.resize(n);
-                return v;
+            if (k_ == k && !stash_.empty()) {
+                const std::size_t got = std::min(n, stash_.size());
+                v.assign(std::make_move_iterator(stash_.end() - got),
+                         std::make_move_iterator(stash_.end()));
+                stash_.erase(stash_.end() - got, stash_.end());
             }
+            if (v.size() < n) pause_ = true;
         }
-        return build(n, k);
+        if (v.size() == n) return v;
+        const std::size_t have = v.size();
+        v.resize(n);
+        HostPool::instance().parallel_for(n - have, 4096, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t i = have + lo; i < have + hi; ++i) v[i].distances_sq.resize(k);
+        });
+        return v;
     }
 
-    /// Schedule the next storage after a call of shape (n, k).
+    /// Schedule the top-up after a call of shape (n, k).
     void refill(std::size_t n, std::size_t k) {
         std::lock_guard<std::mutex> lk(mu_);
         if (k != k_) {
+            doomed_.push_back(std::move(stash_));  // freed on the worker, off the call path
             stash_.clear();
-            ready_ = false;
             k_ = k;
             want_ = 0;
         }
-        want_ = std::max(want_, 2 * n);
         const std::size_t per = sizeof(KnnResult) + k * sizeof(double) + 16;
-        want_ = std::min<std::size_t>(want_, (std::size_t(64) << 20) / per);
-        if (ready_ && stash_.size() >= want_) return;
+        want_ = std::min<std::size_t>(std::max(want_, 4 * n), (std::size_t(64) << 20) / per);
+        if (stash_.size() >= want_ && doomed_.empty()) return;
         pending_ = true;
         cv_.notify_one();
     }
@@ -247,37 +272,40 @@ public:
 private:
     ResultStash() : worker_([this] { loop(); }) {}
 
-    static std::vector<KnnResult> build(std::size_t n, std::size_t k) {
-        std::vector<KnnResult> v(n);
-        HostPool::instance().parallel_for(n, 4096, [&](std::size_t lo, std::size_t hi) {
-            for (std::size_t i = lo; i < hi; ++i) v[i].distances_sq.resize(k);
-        });
-        return v;
-    }
-
+    // The top-up runs on this one worker thread (never the host pool, which
+    // serves the calls) in batches that land in the stash as they finish.
     void loop() {
+        constexpr std::size_t kBatch = 8192;
         std::unique_lock<std::mutex> lk(mu_);
         for (;;) {
             cv_.wait(lk, [&] { return stop_ || pending_; });
             if (stop_) return;
             pending_ = false;
-            const std::size_t n = want_, k = k_;
+            std::vector<std::vector<KnnResult>> doomed = std::move(doomed_);
+            doomed_.clear();
             lk.unlock();
-            std::vector<KnnResult> v(n);  // serial: never holds the host pool
-            for (KnnResult& r : v) r.distances_sq.resize(k);
+            doomed.clear();
             lk.lock();
-            if (k == k_ && n >= stash_.size()) {
-                stash_ = std::move(v);
-                ready_ = true;
+            pause_ = false;
+            while (!stop_ && !pending_ && !pause_ && stash_.size() < want_) {
+                const std::size_t k = k_, n = std::min(kBatch, want_ - stash_.size());
+                lk.unlock();
+                std::vector<KnnResult> v(n);
+                for (KnnResult& r : v) r.distances_sq.resize(k);
+                lk.lock();
+                if (k != k_) continue;
+                for (KnnResult& r : v) stash_.push_back(std::move(r));
             }
         }
     }
 
     std::mutex mu_;
     std::condition_variable cv_;
+    bool pause_ = false;
     std::vector<KnnResult> stash_;
+    std::vector<std::vector<KnnResult>> doomed_;
     std::size_t k_ = 0, want_ = 0;
-    bool ready_ = false, pending_ = false, stop_ = false;
+    bool pending_ = false, stop_ = false;
     std::thread worker_;
 };
 
@@ -329,7 +357,12 @@ inline std::vector<KnnResult> knn_stage(const PointSet& queries, const GridIndex
     detail::HostPool& pool = detail::HostPool::instance();
     detail::ResultStash& stash = detail::ResultStash::instance();
     std::vector<KnnResult> out;
-    std::thread alloc([&] { out = stash.take(n, k_alloc); });
+    const auto t_begin = std::chrono::steady_clock::now();
+    double t_take = 0.0;
+    std::thread alloc([&] {
+        out = stash.take(n, k_alloc);
+        t_take = detail::ms_since(t_begin);
+    });
     struct Join {
         std::thread& t;
         ~Join() {
@@ -356,7 +389,9 @@ inline std::vector<KnnResult> knn_stage(const PointSet& queries, const GridIndex
                            avg.data(), &k_eff, &exhausted, &err),
             err);
     }
+    const double t_call = detail::ms_since(t_begin);
     alloc.join();
+    const double t_join = detail::ms_since(t_begin);
     const auto ke = static_cast<std::size_t>(std::max(k_eff, 0));
     const double* src = d2.p;
     pool.parallel_for(n, 4096, [&](std::size_t lo, std::size_t hi) {
@@ -367,6 +402,9 @@ inline std::vector<KnnResult> knn_stage(const PointSet& queries, const GridIndex
         }
     });
     stash.refill(n, k_alloc);
+    if (detail::host_trace())
+        std::fprintf(stderr, "[aidw knn_stage] n %zu: results ready %.3f, C-ABI %.3f, joined %.3f, "
+                     "materialised %.3f ms\n", n, t_take, t_call, t_join, detail::ms_since(t_begin));
     return out;
 }
 

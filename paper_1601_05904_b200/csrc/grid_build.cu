@@ -5,7 +5,8 @@
 // scatter).  Here the same CSR arrays come from
 //   1. cell_ids_kernel  : FP64 locate_cell per point (exact reference
 //                         rounding), key = row-major cell id, value = index,
-//                         per-cell histogram with global atomics;
+//                         per-cell histogram with global atomics; two points
+//                         per thread through double2 loads / uint2 stores;
 //   2. exclusive_scan   : cell_start = exclusive prefix of the histogram
 //                         (single pass, decoupled look-back);
 //   3. counting sort    : scatter through per-cell atomic cursors, then each
@@ -38,23 +39,58 @@ constexpr int kSortTile = kSortThreads * kSortItems;  // 2048 keys
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kThreads * kScanItems;  // 2048 values
 
+// Two points per thread: 16-byte (double2) coordinate loads and 8-byte
+// (uint2) key / value stores when the arrays are aligned for them (device
+// pointers handed in through aidw_run_pipeline_device may not be).
+__device__ __forceinline__ uint32_t cell_of(double x, double y, const GridGeom& g, size_t i,
+                                            uint32_t* counts, long long* fail) {
+    int col, row;
+    if (locate_cell_dev(x, y, g, col, row)) {
+        const uint32_t cell = static_cast<uint32_t>(row) * static_cast<uint32_t>(g.n_col) +
+                              static_cast<uint32_t>(col);
+        if (counts) atomicAdd(&counts[cell], 1u);
+        return cell;
+    }
+    atomicMin(fail, static_cast<long long>(i));
+    return 0;
+}
+
+template <bool VEC>
 __global__ void cell_ids_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                 size_t m, GridGeom g, uint32_t* __restrict__ keys,
                                 uint32_t* __restrict__ vals, uint32_t* __restrict__ counts,
                                 long long* __restrict__ fail) {
-    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t i = 2 * (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x);
     if (i >= m) return;
-    int col, row;
-    uint32_t cell = 0;
-    if (locate_cell_dev(x[i], y[i], g, col, row)) {
-        cell = static_cast<uint32_t>(row) * static_cast<uint32_t>(g.n_col) +
-               static_cast<uint32_t>(col);
-        if (counts) atomicAdd(&counts[cell], 1u);
-    } else {
-        atomicMin(fail, static_cast<long long>(i));
+    if (VEC && i + 1 < m) {
+        const double2 px = reinterpret_cast<const double2*>(x)[i / 2];
+        const double2 py = reinterpret_cast<const double2*>(y)[i / 2];
+        const uint32_t c0 = cell_of(px.x, py.x, g, i, counts, fail);
+        const uint32_t c1 = cell_of(px.y, py.y, g, i + 1, counts, fail);
+        reinterpret_cast<uint2*>(keys)[i / 2] = make_uint2(c0, c1);
+        if (vals)
+            reinterpret_cast<uint2*>(vals)[i / 2] =
+                make_uint2(static_cast<uint32_t>(i), static_cast<uint32_t>(i + 1));
+        return;
     }
-    keys[i] = cell;
-    if (vals) vals[i] = static_cast<uint32_t>(i);
+    for (size_t j = i; j < i + 2 && j < m; ++j) {
+        keys[j] = cell_of(x[j], y[j], g, j, counts, fail);
+        if (vals) vals[j] = static_cast<uint32_t>(j);
+    }
+}
+
+void launch_cell_ids(const double* x, const double* y, size_t m, const GridGeom& g,
+                     uint32_t* keys, uint32_t* vals, uint32_t* counts, long long* fail,
+                     cudaStream_t s) {
+    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(vals)) & 7) == 0;
+    const size_t threads = ceil_div(m, static_cast<size_t>(2));
+    if (vec)
+        LAUNCH(cell_ids_kernel<true>, ceil_div(threads, kThreads), kThreads, 0, s, x, y, m, g,
+               keys, vals, counts, fail);
+    else
+        LAUNCH(cell_ids_kernel<false>, ceil_div(threads, kThreads), kThreads, 0, s, x, y, m, g,
+               keys, vals, counts, fail);
 }
 
 __global__ void interleave_kernel(const double* __restrict__ x, const double* __restrict__ y,
@@ -619,8 +655,7 @@ void build_grid_device(const double* d_x, const double* d_y, size_t m,
         nbig(2, s);
     CK(cudaMemsetAsync(out.cell_start.get(), 0, (cells + 1) * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(nbig.get(), 0, 2 * sizeof(uint32_t), s));
-    LAUNCH(cell_ids_kernel, ceil_div(m, kThreads), kThreads, 0, s, d_x, d_y, m, g, keys.get(),
-           static_cast<uint32_t*>(nullptr), out.cell_start.get(), d_fail);
+    launch_cell_ids(d_x, d_y, m, g, keys.get(), nullptr, out.cell_start.get(), d_fail, s);
     // counting sort: cursors start at cell_start (written by the same scan,
     // cells + 1 entries); vals receives the scatter
     exclusive_scan_u32(out.cell_start.get(), out.cell_start.get(), cells + 1, s, cursor.get());
@@ -641,8 +676,7 @@ void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, cons
     perm.alloc(n, s);
     cells.alloc(n, s);
     if (n == 0) return;
-    LAUNCH(cell_ids_kernel, ceil_div(n, kThreads), kThreads, 0, s, d_qx, d_qy, n, g,
-           cells.get(), perm.get(), static_cast<uint32_t*>(nullptr), d_fail);
+    launch_cell_ids(d_qx, d_qy, n, g, cells.get(), perm.get(), nullptr, d_fail, s);
     const size_t total = static_cast<size_t>(g.n_col) * static_cast<size_t>(g.n_row);
     // the cell order only buys locality (every query's result is independent
     // of the visiting order): few queries are bucketed by their key's top bits

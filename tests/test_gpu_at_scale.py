@@ -16,7 +16,8 @@ SURVEY §8(d) "Parity set":
     fractional-alpha queries) — the GPU interpolates all 1M queries, the
     reference the sample plus the queries that pin bbox(data ∪ queries), so
     both see the same grid, area and snap tolerance;
-  * configs[4] (4M planar data, 4096^2 raster lattice, k = 15): the full
+  * configs[4] (4M planar data, 4096^2 raster lattice, k = 15): kNN of all
+    16.8M lattice queries against the reference's knn_stage; the full
     raster on the GPU (aidw_run_raster), >= 4096 lattice points spread over
     every row checked against the reference (the lattice lies inside
     bbox(data), so bbox, area and snap tolerance are the raster's).
@@ -205,6 +206,38 @@ def test_pipeline_1m_stratified_sample():
     out64 = A.run_pipeline(data, q, A.RunConfig(params=A.AidwParams(k=10)))
     assert np.array_equal(out64.result.alphas, alpha)
     assert rel_err(out64.result.predicted[s], ref_pred) <= FP64_TOL
+
+
+# ------------------------------------------------------------------ DEM kNN, full
+def test_dem_knn_stage_all_lattice_queries():
+    """configs[4] kNN in full: all 4096^2 lattice queries over 4M planar
+    points, k = 15 — d2 lists and averages bit-identical to the reference's
+    knn_stage (knn.hpp:255-271); (d2, idx) index sets against the C oracle on
+    every 16th lattice row (the oracle is single-pass C: bounded time)."""
+    need_ref()
+    nx = ny = 4096
+    k = 15
+    xs, ys, _ = O.generate_points(4_000_000, UNIT, 42, 1)
+    bb = O.compute_bbox(xs, ys)
+    qx, qy = O.raster_lattice(nx, ny, bb)
+    assert np.array_equal(O.compute_bbox(xs, ys, qx, qy), bb)
+    cfg_o = O.make_grid_config(bb, O.choose_cell_width(xs.size, bb, 4.0))
+    cfg = A.GridConfig(cfg_o.cell_width, cfg_o.n_col, cfg_o.n_row, cfg_o.min_x, cfg_o.min_y)
+    index = A.build_index(A.PointSet(xs, ys), cfg)
+    got = A.knn_stage(A.PointSet(qx, qy), index, A.PointSet(xs, ys), k)
+    ref_d2, ref_avg, ref_exh, ref_len = O.ref_knn_stage(qx, qy, xs, ys, k, factor=4.0,
+                                                        workers=THREADS)
+    assert np.all(ref_len == k) and not ref_exh.any() and not got.exhausted
+    assert np.array_equal(got.distances_sq, ref_d2)
+    assert np.array_equal(got.average_distance, ref_avg)
+    del ref_d2, ref_avg
+    grid_o = O.build_index(xs, ys, cfg_o)
+    assert np.array_equal(index.sorted_point_ids, grid_o[0])
+    rows = np.arange(0, ny, 16)
+    sel = (rows[:, None] * nx + np.arange(nx)[None, :]).ravel()
+    o_d2, o_ids, _ = oracle_knn_parallel(qx[sel], qy[sel], cfg_o, grid_o, xs.size, k)
+    assert np.array_equal(got.distances_sq[sel], o_d2)
+    assert np.array_equal(got.indices[sel], o_ids)
 
 
 # ------------------------------------------------------------------ DEM raster

@@ -28,7 +28,7 @@ template <int MODE> __global__ void k(float* out, float s) {
       if (MODE == 1) p[i] = ffma2(p[i], ps, ps);                     // FFMA2
       if (MODE == 2) p[i] = fadd2(p[i], ps);                         // FADD2
       if (MODE == 3) a[i] = ex2(a[i]);                               // MUFU.EX2
-      if (MODE == 4) a[i] = rcp(a[i]);                               // MUFU.RCP
+      if (MODE == 4) a[i] = __int_as_float(__float_as_int(rcp(a[i])) ^ 1);  // MUFU.RCP (+ LOP3: rcp(rcp(x)) folds away)
       if (MODE == 5) a[i] = lg2(a[i]);                               // MUFU.LG2
       if (MODE == 6) { p[i] = ffma2(p[i], ps, ps); a[i] = ex2(a[i]); }  // FFMA2 + EX2 mix
       if (MODE == 7) { a[i] = fmaf(a[i], s, 0.5f); a[i] = a[i] + s; }   // FFMA + FADD
