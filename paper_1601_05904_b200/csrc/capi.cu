@@ -322,13 +322,14 @@ void nearest_search(const double* d_dx, const double* d_dy, size_t m, const doub
     build_grid_device(d_dx, d_dy, m, cfg, g, fails.slot(kFailData), s);
     DBuf<uint32_t> qcell;
     const GridGeom geom = make_geom(cfg);
-    sort_queries_by_cell(d_qx, d_qy, n, geom, out.perm, qcell, fails.slot(kFailQuery), s);
+    const int nbc = sort_queries_by_cell(d_qx, d_qy, n, geom, out.perm, qcell, fails.slot(kFailQuery), s);
     a.g = geom;
     a.cell_start = g.cell_start.get();
     a.sorted_ids = g.sorted_ids.get();
     a.sorted_xy = g.sorted_xy.get();
     a.perm = out.perm.get();
     a.qcell = qcell.get();
+    a.qkey_nbc = nbc;
     run_knn_grid(a, s);
 }
 
@@ -567,7 +568,7 @@ void enqueue_pass(const PassPlan& pl, const PipelineIO& io, const aidw_run_confi
         build_grid_device(io.dx, io.dy, m, pl.gc, g, fails.slot(kFailData), s);
         record(pe.build1, s);
         const GridGeom geom = make_geom(pl.gc);
-        sort_queries_by_cell(io.qx, io.qy, n, geom, perm, qcell, fails.slot(kFailQuery), s);
+        a.qkey_nbc = sort_queries_by_cell(io.qx, io.qy, n, geom, perm, qcell, fails.slot(kFailQuery), s);
         a.g = geom;
         a.cell_start = g.cell_start.get();
         a.sorted_ids = g.sorted_ids.get();
@@ -1268,7 +1269,7 @@ void knn_grid_stage(const double* qx, const double* qy, size_t n, const aidw_gri
     h2d(dqx, qx, n, s);
     h2d(dqy, qy, n, s);
     const GridGeom geom = make_geom(cfg);
-    sort_queries_by_cell(dqx.get(), dqy.get(), n, geom, perm, qcell, fails.slot(kFailQuery), s);
+    const int nbc = sort_queries_by_cell(dqx.get(), dqy.get(), n, geom, perm, qcell, fails.slot(kFailQuery), s);
     KnnArgs a;
     a.qx = dqx.get();
     a.qy = dqy.get();
@@ -1285,6 +1286,7 @@ void knn_grid_stage(const double* qx, const double* qy, size_t n, const aidw_gri
     a.sorted_xy = d_xy;
     a.perm = perm.get();
     a.qcell = qcell.get();
+    a.qkey_nbc = nbc;
     // a query outside the grid makes K2 skip it (locate fails the same way
     // in both kernels); the error is raised after the single synchronisation
     run_knn_grid(a, s);

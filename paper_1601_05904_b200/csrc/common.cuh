@@ -123,6 +123,35 @@ struct GridGeom {
     double lo_x, hi_x, lo_y, hi_y;
 };
 
+// Query visiting order of K2: cells in 8 x 8-cell blocks, blocks row-major,
+// cells row-major inside a block, so 128 consecutive queries cover a compact
+// square of cells (row-major cell ids give a one-row strip).  nbc = blocks
+// per grid row; 0 = plain row-major ids (key range would not fit 32 bits).
+constexpr int kQBlockBits = 3;
+inline int query_block_cols(int n_col, int n_row) {
+    const uint64_t nbc = (static_cast<uint64_t>(n_col) + 7) >> kQBlockBits;
+    const uint64_t nbr = (static_cast<uint64_t>(n_row) + 7) >> kQBlockBits;
+    return nbc * nbr * 64 <= 0xFFFFFFFFull ? static_cast<int>(nbc) : 0;
+}
+__host__ __device__ __forceinline__ uint32_t query_key(int row, int col, int n_col, int nbc) {
+    if (nbc == 0) return static_cast<uint32_t>(row) * static_cast<uint32_t>(n_col) + static_cast<uint32_t>(col);
+    const uint32_t b = static_cast<uint32_t>(row >> kQBlockBits) * static_cast<uint32_t>(nbc) +
+                       static_cast<uint32_t>(col >> kQBlockBits);
+    return (b << (2 * kQBlockBits)) | (static_cast<uint32_t>(row & 7) << kQBlockBits) |
+           static_cast<uint32_t>(col & 7);
+}
+__host__ __device__ __forceinline__ void query_cell(uint32_t key, int n_col, int nbc, int& row,
+                                                    int& col) {
+    if (nbc == 0) {
+        col = static_cast<int>(key % static_cast<uint32_t>(n_col));
+        row = static_cast<int>(key / static_cast<uint32_t>(n_col));
+        return;
+    }
+    const uint32_t b = key >> (2 * kQBlockBits);
+    row = static_cast<int>((b / static_cast<uint32_t>(nbc)) << kQBlockBits) + static_cast<int>((key >> kQBlockBits) & 7);
+    col = static_cast<int>((b % static_cast<uint32_t>(nbc)) << kQBlockBits) + static_cast<int>(key & 7);
+}
+
 inline GridGeom make_geom(const aidw_grid_config& c) {
     GridGeom g;
     g.cell_width = c.cell_width;
@@ -198,8 +227,9 @@ void build_grid_device(const double* d_x, const double* d_y, size_t m,
 void interleave_xy(const double* d_x, const double* d_y, size_t n, double2* d_xy, cudaStream_t s);
 
 // Sort n query points by cell: returns the permutation (sorted position ->
-// query index) and the sorted cell ids; failures -> *d_fail.
-void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, const GridGeom& g,
+// query index) and the sorted query keys (query_key, block-major cells);
+// the result is the keys' nbc (blocks per grid row); failures -> *d_fail.
+int sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, const GridGeom& g,
                           DBuf<uint32_t>& perm, DBuf<uint32_t>& cells, long long* d_fail,
                           cudaStream_t s);
 

@@ -42,12 +42,13 @@ constexpr int kScanTile = kThreads * kScanItems;  // 2048 values
 // Two points per thread: 16-byte (double2) coordinate loads and 8-byte
 // (uint2) key / value stores when the arrays are aligned for them (device
 // pointers handed in through aidw_run_pipeline_device may not be).
+// key: the row-major cell id (nbc = 0; data points, histogrammed into
+// counts) or the block-major query key (query_key)
 __device__ __forceinline__ uint32_t cell_of(double x, double y, const GridGeom& g, size_t i,
-                                            uint32_t* counts, long long* fail) {
+                                            uint32_t* counts, long long* fail, int nbc) {
     int col, row;
     if (locate_cell_dev(x, y, g, col, row)) {
-        const uint32_t cell = static_cast<uint32_t>(row) * static_cast<uint32_t>(g.n_col) +
-                              static_cast<uint32_t>(col);
+        const uint32_t cell = query_key(row, col, g.n_col, nbc);
         if (counts) atomicAdd(&counts[cell], 1u);
         return cell;
     }
@@ -59,14 +60,14 @@ template <bool VEC>
 __global__ void cell_ids_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                 size_t m, GridGeom g, uint32_t* __restrict__ keys,
                                 uint32_t* __restrict__ vals, uint32_t* __restrict__ counts,
-                                long long* __restrict__ fail) {
+                                long long* __restrict__ fail, int nbc) {
     const size_t i = 2 * (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x);
     if (i >= m) return;
     if (VEC && i + 1 < m) {
         const double2 px = reinterpret_cast<const double2*>(x)[i / 2];
         const double2 py = reinterpret_cast<const double2*>(y)[i / 2];
-        const uint32_t c0 = cell_of(px.x, py.x, g, i, counts, fail);
-        const uint32_t c1 = cell_of(px.y, py.y, g, i + 1, counts, fail);
+        const uint32_t c0 = cell_of(px.x, py.x, g, i, counts, fail, nbc);
+        const uint32_t c1 = cell_of(px.y, py.y, g, i + 1, counts, fail, nbc);
         reinterpret_cast<uint2*>(keys)[i / 2] = make_uint2(c0, c1);
         if (vals)
             reinterpret_cast<uint2*>(vals)[i / 2] =
@@ -74,23 +75,23 @@ __global__ void cell_ids_kernel(const double* __restrict__ x, const double* __re
         return;
     }
     for (size_t j = i; j < i + 2 && j < m; ++j) {
-        keys[j] = cell_of(x[j], y[j], g, j, counts, fail);
+        keys[j] = cell_of(x[j], y[j], g, j, counts, fail, nbc);
         if (vals) vals[j] = static_cast<uint32_t>(j);
     }
 }
 
 void launch_cell_ids(const double* x, const double* y, size_t m, const GridGeom& g,
                      uint32_t* keys, uint32_t* vals, uint32_t* counts, long long* fail,
-                     cudaStream_t s) {
+                     cudaStream_t s, int nbc = 0) {
     const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0 &&
                      ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(vals)) & 7) == 0;
     const size_t threads = ceil_div(m, static_cast<size_t>(2));
     if (vec)
         LAUNCH(cell_ids_kernel<true>, ceil_div(threads, kThreads), kThreads, 0, s, x, y, m, g,
-               keys, vals, counts, fail);
+               keys, vals, counts, fail, nbc);
     else
         LAUNCH(cell_ids_kernel<false>, ceil_div(threads, kThreads), kThreads, 0, s, x, y, m, g,
-               keys, vals, counts, fail);
+               keys, vals, counts, fail, nbc);
 }
 
 __global__ void interleave_kernel(const double* __restrict__ x, const double* __restrict__ y,
@@ -670,19 +671,22 @@ void build_grid_device(const double* d_x, const double* d_y, size_t m,
            out.sorted_ids.get(), out.sorted_xy.get(), out.sorted_x.get(), out.sorted_y.get());
 }
 
-void sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, const GridGeom& g,
-                          DBuf<uint32_t>& perm, DBuf<uint32_t>& cells, long long* d_fail,
-                          cudaStream_t s) {
+int sort_queries_by_cell(const double* d_qx, const double* d_qy, size_t n, const GridGeom& g,
+                         DBuf<uint32_t>& perm, DBuf<uint32_t>& cells, long long* d_fail,
+                         cudaStream_t s) {
     perm.alloc(n, s);
     cells.alloc(n, s);
-    if (n == 0) return;
-    launch_cell_ids(d_qx, d_qy, n, g, cells.get(), perm.get(), nullptr, d_fail, s);
-    const size_t total = static_cast<size_t>(g.n_col) * static_cast<size_t>(g.n_row);
+    const int nbc = query_block_cols(g.n_col, g.n_row);
+    if (n == 0) return nbc;
+    launch_cell_ids(d_qx, d_qy, n, g, cells.get(), perm.get(), nullptr, d_fail, s, nbc);
+    const size_t total = nbc ? static_cast<size_t>(nbc) * ((static_cast<size_t>(g.n_row) + 7) >> kQBlockBits) * 64
+                             : static_cast<size_t>(g.n_col) * static_cast<size_t>(g.n_row);
     // the cell order only buys locality (every query's result is independent
     // of the visiting order): few queries are bucketed by their key's top bits
     // in one launch instead of the six of the two radix passes
     if (n <= small_sort_n()) bucket_by_key_small(cells.get(), perm.get(), n, bits_for(total - 1), s);
     else radix_sort_pairs(cells.get(), perm.get(), n, bits_for(total - 1), s);
+    return nbc;
 }
 
 // One CTA groups up to kSmallSortMax (key, value) pairs by the top B <= 12

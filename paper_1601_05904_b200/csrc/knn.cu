@@ -3,10 +3,16 @@
 // Replaces knn_stage / grid_knn (proj/include/aidw/knn.hpp:130-271) and the
 // per-query adaptive_alpha chain (adaptive.hpp:20-116).
 //
-// One thread per query; queries are visited in cell-sorted order (radix
-// sort in grid_build.cu) so a warp's 32 queries scan overlapping cell
-// blocks and the candidate loads hit L1; each thread walks its cells as one
-// level block row by row (a row segment of cells is contiguous in memory).  The search is the reference's:
+// One thread per query; queries are visited in block-major cell order
+// (8 x 8-cell blocks, radix sort in grid_build.cu) so a CTA's 128 queries
+// sit in a compact patch of cells: the CTA stages the patch widened by two
+// cells (coordinates, ids, local CSR offsets) in shared memory and its
+// threads scan the row segments inside it from there (measured: -1.3 % K2
+// time clustered, +1.5-2.5 % uniform / stress / DEM — K2 is bound by its
+// top-k network, not by candidate loads, profiles/r02/k2_stage_s43.txt);
+// segments outside the patch read global memory through L1.  Each thread
+// walks its cells as one level block row by row (a row segment of cells is
+// contiguous in memory).  The search is the reference's:
 // expansion level = smallest L0 whose clipped (2L0+1)^2 block holds >= k
 // points, plus one; scan that block; widen ring by ring until
 // kth <= (L*w)^2 (1 - 1e-9) or the block covers the grid.  The block is
@@ -32,7 +38,9 @@
 
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "knn.cuh"
@@ -255,6 +263,106 @@ __device__ __forceinline__ void finish_query(const KnnArgs& a, TopK& t, size_t p
     }
 }
 
+// ---------------------------------------------------------------- staging
+// The CTA's cell neighbourhood in shared memory.  A CTA's 128 queries are
+// consecutive in the block-major visiting order (query_key), so their cells
+// form a compact patch; the patch widened by kStageMargin cells (the first
+// block of a uniform k = 10 query is its 5 x 5 cells) is copied once —
+// coordinates, ids and the local CSR offsets of every cell — and every row
+// segment inside it is scanned from shared memory.  Segments outside it
+// (wider blocks, rings) read global memory as before; which source a
+// candidate comes from never changes the candidates or their order.
+constexpr int kStageMargin = 2;
+constexpr int kStagePts = 1536;   // 30 KB of {x, y, id}
+constexpr int kStageCells = 1024; // local CSR entries (rows x (cols + 1))
+constexpr int kStageRows = 64;
+
+struct KnnStage {
+    double2 xy[kStagePts];
+    uint32_t id[kStagePts];
+    uint32_t lcs[kStageCells];     // local offset of cell (r, c) of the patch, c in [C0, C1 + 1]
+    uint32_t row_base[kStageRows + 1];
+    uint32_t row_g[kStageRows];    // global CSR offset of the row segment's first point
+    int r0, r1, c0, c1, on;
+    int red[4][4];
+};
+
+// All threads of the CTA; valid: the thread holds a query at (row, col).
+__device__ void stage_patch(const KnnArgs& a, KnnStage& st, bool valid, int row, int col) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int v[4] = {valid ? row : INT_MAX, valid ? -row : INT_MAX, valid ? col : INT_MAX,
+                valid ? -col : INT_MAX};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[i] = min(v[i], __shfl_xor_sync(0xFFFFFFFFu, v[i], o));
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) st.red[warp][i] = v[i];
+    __syncthreads();
+    if (tid == 0) {
+        int m[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
+            for (int i = 0; i < 4; ++i) m[i] = min(m[i], st.red[w][i]);
+        st.on = 0;
+        if (m[0] != INT_MAX) {
+            st.r0 = max(0, m[0] - kStageMargin), st.r1 = min(a.g.n_row - 1, -m[1] + kStageMargin);
+            st.c0 = max(0, m[2] - kStageMargin), st.c1 = min(a.g.n_col - 1, -m[3] + kStageMargin);
+            const int nr = st.r1 - st.r0 + 1, nc = st.c1 - st.c0 + 2;
+            st.on = nr <= kStageRows && nr * nc <= kStageCells;
+        }
+    }
+    __syncthreads();
+    if (!st.on) return;
+    const int nr = st.r1 - st.r0 + 1, nc = st.c1 - st.c0 + 2;  // nc: cells + 1 boundaries
+    for (int i = tid; i < nr * nc; i += blockDim.x) {
+        const int r = i / nc, c = i - r * nc;
+        st.lcs[i] = __ldg(a.cell_start + static_cast<size_t>(st.r0 + r) * a.g.n_col + st.c0 + c);
+    }
+    __syncthreads();
+    if (warp == 0) {  // row lengths -> exclusive prefix (rows <= 64: two warp passes)
+        uint32_t carry = 0;
+        for (int r0 = 0; r0 < nr; r0 += 32) {
+            const int r = r0 + lane;
+            const uint32_t len = r < nr ? st.lcs[r * nc + nc - 1] - st.lcs[r * nc] : 0u;
+            uint32_t inc = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            if (r < nr) {
+                st.row_base[r] = carry + inc - len;
+                st.row_g[r] = st.lcs[r * nc];
+            }
+            carry += __shfl_sync(0xFFFFFFFFu, inc, 31);
+        }
+        if (lane == 0) {
+            st.row_base[nr] = carry;
+            if (carry > static_cast<uint32_t>(kStagePts)) st.on = 0;
+        }
+    }
+    __syncthreads();
+    if (!st.on) return;
+    for (int i = tid; i < nr * nc; i += blockDim.x) {  // global CSR -> local offsets
+        const int r = i / nc;
+        st.lcs[i] = st.row_base[r] + (st.lcs[i] - st.row_g[r]);
+    }
+    const uint32_t total = st.row_base[nr];
+    for (uint32_t f = tid; f < total; f += blockDim.x) {
+        int lo = 0, hi = nr - 1;  // the row holding local point f
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (st.row_base[mid] <= f) lo = mid;
+            else hi = mid - 1;
+        }
+        const uint32_t g = st.row_g[lo] + (f - st.row_base[lo]);
+        st.xy[f] = __ldg(a.sorted_xy + g);
+        st.id[f] = __ldg(a.sorted_ids + g);
+    }
+    __syncthreads();
+}
+
 // Points of row rr, cells [c0, c1] (clipped to the grid): contiguous in the
 // cell-sorted arrays (row-major cells), so one cell_start round trip and one
 // loop cover the whole segment.  Once the buffer is full the segment is
@@ -264,9 +372,10 @@ __device__ __forceinline__ void finish_query(const KnnArgs& a, TopK& t, size_t p
 // ever keeps more cells than the exact test, so results are unchanged).
 // The next candidate's coordinates and id are loaded one iteration ahead.
 template <class TopK>
-__device__ __forceinline__ void scan_row(const KnnArgs& a, TopK& t, double qx, double qy,
-                                         double fx, double fy, double inv_w2, int rr, int c0,
-                                         int c1, uint32_t& snap, unsigned long long& scanned) {
+__device__ __forceinline__ void scan_row(const KnnArgs& a, const KnnStage* st, TopK& t, double qx,
+                                         double qy, double fx, double fy, double inv_w2, int rr,
+                                         int c0, int c1, uint32_t& snap,
+                                         unsigned long long& scanned) {
     const int n_col = a.g.n_col, n_row = a.g.n_row;
     if (t.full()) {
         const double inf = __longlong_as_double(0x7FF0000000000000ll);
@@ -290,6 +399,20 @@ __device__ __forceinline__ void scan_row(const KnnArgs& a, TopK& t, double qx, d
         if (c1 == n_col - 1 && k0 > n_col - 1) k0 = n_col - 1;
         c0 = k0, c1 = k1;
         if (c0 > c1) return;
+    }
+    if (st && rr >= st->r0 && rr <= st->r1 && c0 >= st->c0 && c1 <= st->c1) {
+        const uint32_t* lcs = st->lcs + (rr - st->r0) * (st->c1 - st->c0 + 2) - st->c0;
+        uint32_t s = lcs[c0];
+        const uint32_t e = lcs[c1 + 1];
+        scanned += e - s;
+        for (; s < e; ++s) {
+            const double2 cxy = st->xy[s];
+            const uint32_t cid = st->id[s];
+            const double cd = dsq_rn(qx, qy, cxy.x, cxy.y);
+            if (cd <= a.snap_sq) snap = cid < snap ? cid : snap;
+            if (t.admits(cd)) t.insert(cd, cid);
+        }
+        return;
     }
     const size_t base = static_cast<size_t>(rr) * static_cast<size_t>(n_col);
     uint32_t s = __ldg(a.cell_start + base + c0);
@@ -316,15 +439,20 @@ __device__ __forceinline__ void scan_row(const KnnArgs& a, TopK& t, double qx, d
 // One thread per query.
 template <class TopK>
 __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
+    __shared__ KnnStage stage;
     const size_t pos = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     unsigned long long scanned = 0, ref_scanned = 0;
+    int col = 0, row = 0;
+    if (pos < a.n) query_cell(a.qcell[pos], a.g.n_col, a.qkey_nbc, row, col);
+    const KnnStage* stp = nullptr;
+    if (a.stage) {
+        stage_patch(a, stage, pos < a.n, row, col);
+        if (stage.on) stp = &stage;
+    }
     if (pos < a.n) {
         const uint32_t qi = a.perm[pos];
         const double qx = a.qx[qi], qy = a.qy[qi];
-        const uint32_t cell = a.qcell[pos];
         const int n_col = a.g.n_col, n_row = a.g.n_row;
-        const int col = static_cast<int>(cell % static_cast<uint32_t>(n_col));
-        const int row = static_cast<int>(cell / static_cast<uint32_t>(n_col));
 
         // expansion level (knn.hpp:130-156)
         int level;
@@ -374,7 +502,7 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
             for (int d = 0; d <= 2 * level; ++d) {
                 const int rr = row + ((d & 1) ? -((d + 1) >> 1) : (d >> 1));
                 if (rr < 0 || rr >= n_row) continue;
-                scan_row(a, t, qx, qy, fx, fy, inv_w2, rr, c0, c1, snap, scanned);
+                scan_row(a, stp, t, qx, qy, fx, fy, inv_w2, rr, c0, c1, snap, scanned);
             }
         }
         // ring widening (knn.hpp:234-247, scan_ring :175-194)
@@ -396,15 +524,15 @@ __global__ void __launch_bounds__(128) knn_grid_kernel(KnnArgs a) {
                 rect_count(a, c0, c1, imax(0, row - r), imin(n_row - 1, row + r)) ==
                     rect_count(a, imax(0, col - r + 1), imin(n_col - 1, col + r - 1), r0, r1))
                 continue;
-            if (row - r >= 0) scan_row(a, t, qx, qy, fx, fy, inv_w2, row - r, c0, c1, snap, scanned);
+            if (row - r >= 0) scan_row(a, stp, t, qx, qy, fx, fy, inv_w2, row - r, c0, c1, snap, scanned);
             if (row + r <= n_row - 1)
-                scan_row(a, t, qx, qy, fx, fy, inv_w2, row + r, c0, c1, snap, scanned);
+                scan_row(a, stp, t, qx, qy, fx, fy, inv_w2, row + r, c0, c1, snap, scanned);
             if (col - r >= 0 && (!a.rect_prefix || rect_count(a, col - r, col - r, r0, r1) > 0))
                 for (int rr = r0; rr <= r1; ++rr)
-                    scan_row(a, t, qx, qy, fx, fy, inv_w2, rr, col - r, col - r, snap, scanned);
+                    scan_row(a, stp, t, qx, qy, fx, fy, inv_w2, rr, col - r, col - r, snap, scanned);
             if (col + r <= n_col - 1 && (!a.rect_prefix || rect_count(a, col + r, col + r, r0, r1) > 0))
                 for (int rr = r0; rr <= r1; ++rr)
-                    scan_row(a, t, qx, qy, fx, fy, inv_w2, rr, col + r, col + r, snap, scanned);
+                    scan_row(a, stp, t, qx, qy, fx, fy, inv_w2, rr, col + r, col + r, snap, scanned);
         }
         if (a.ref_candidates) {  // what the reference scanned: the final-level block
             ref_scanned = rect_count(a, imax(0, col - level), imin(n_col - 1, col + level),
@@ -527,6 +655,11 @@ __global__ void __launch_bounds__(kPrefixThreads) rect_prefix_kernel(
 
 void run_knn_grid(KnnArgs a, cudaStream_t s) {
     if (a.n == 0) return;
+    static const int stage_env = [] {  // AIDW_K2_STAGE=0: no shared-memory staging (A/B)
+        const char* v = std::getenv("AIDW_K2_STAGE");
+        return v ? std::atoi(v) : 1;
+    }();
+    a.stage = a.stage && stage_env;
     DBuf<uint32_t> prefix;
     if (!a.rect_prefix && a.m >= static_cast<size_t>(a.k)) {
         prefix.alloc((static_cast<size_t>(a.g.n_row) + 1) * (static_cast<size_t>(a.g.n_col) + 1), s);

@@ -36,7 +36,9 @@ struct KnnArgs {
     const double* qx = nullptr;
     const double* qy = nullptr;
     const uint32_t* perm = nullptr;
-    const uint32_t* qcell = nullptr;
+    const uint32_t* qcell = nullptr;  // query keys (query_key: block-major, qkey_nbc blocks/row)
+    int qkey_nbc = 0;
+    int stage = 1;  // stage the CTA's cell patch in shared memory (AIDW_K2_STAGE=0: off)
     size_t n = 0;
     int k = 1;       // requested
     int k_eff = 1;   // min(k, m)
