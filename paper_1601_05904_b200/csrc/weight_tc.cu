@@ -520,8 +520,11 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const Smem& sm, uint32
             else near_tile<MODE>(nf, q, qc, nw, nz);
             if (nq) SW += nw, SWZ += nz;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.bempty[s]);
+        // every lane releases the stage after its own reads (an arrival by
+        // lane 0 after __syncwarp is as correct — the release is cumulative —
+        // but racecheck does not see it; same K4 time,
+        // profiles/r02/tc_release_s47.txt)
+        mbar_arrive(&sm.bempty[s]);
         if (t + 2 < T) {  // A(t + 2): the MMAs of tile t (its last readers) are complete
             build_a(myabuf + (t & 1) * kABytes, r, q, __ldg(a.tile_geo + t0 + t + 2));
             fence_proxy_async();
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) weight_tc_kernel(TcArgs a) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.bfull[s], 1);
-            mbar_init(&sm.bempty[s], kGroups + kEpiWarps);
+            mbar_init(&sm.bempty[s], kGroups + kEpiWarps * 32);
         }
         for (int i = 0; i < 2 * kGroups; ++i) mbar_init(&sm.afull[i], 4);
         for (int i = 0; i < kBufs * kGroups; ++i) {

@@ -1,7 +1,8 @@
 """Small end-to-end runs for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): the fused pipeline (FP32 and FP64 weighting, aidw and
 idw), the drop-in batch calls, the raster path, a crowded-cell grid, the recipe
-classes (alpha = 1, 2, 3, 4, mixed warps) and the per-call workspace reuse."""
+classes (alpha = 1, 2, 3, 4, mixed warps), the per-call workspace reuse, and
+the tensor-core K4 engine (m >= 64K) with its side-stream CUDA-core launch."""
 import os
 import sys
 
@@ -31,4 +32,10 @@ xs = np.concatenate([np.full(5000, 0.5), np.random.default_rng(0).random(2000)])
 ys = np.concatenate([np.full(5000, 0.5), np.random.default_rng(1).random(2000)])
 zs = np.arange(7000, dtype=np.float64)
 A.run_pipeline(A.PointSet(xs, ys, zs), q, A.RunConfig(params=A.AidwParams(k=10)))
+# m >= 64K: the tensor-core K4 engine (recipe queries) beside the CUDA-core
+# launch (general-alpha queries) on its side stream
+big = A.generate_random_points(70_000, UNIT, 7)
+A.run_pipeline(big, A.generate_random_queries(1500, UNIT, 8), A.RunConfig(params=A.AidwParams(k=10)))
+A.run_pipeline(A.generate_clustered(70_000, seed=9), A.generate_clustered(1200, seed=10, with_values=False),
+               A.RunConfig(params=A.AidwParams(k=10, alpha_levels=(1.0, 1.0, 2.0, 3.0, 4.0))))
 print("sanitize run ok")
