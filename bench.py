@@ -21,7 +21,7 @@ FP64 weighting kernel (the reference's precision).
 (oracle/_ref/libaidw_ref.so, compiled in place from /root/reference) on all
 host threads, on inputs made by the reference's own generator — this arm
 never loads the repo's library.  Each timed step is a full pass over all n
-queries when K full passes fit AIDW_REF_BUDGET_S (default 1500 s); otherwise
+queries when K full passes fit AIDW_REF_BUDGET_S (default 300 s); otherwise
 each step interpolates a fixed strided query sample and the line reports the
 throughput measured on it (`cpu_baseline.sampled`).
 """
@@ -333,7 +333,7 @@ def run_reference_arm(args, cfg):
     queries = (np.concatenate([p[1][0] for p in parts]), np.concatenate([p[1][1] for p in parts]))
     del parts
     n = queries[0].size
-    budget = float(os.environ.get("AIDW_REF_BUDGET_S", "1500"))
+    budget = float(os.environ.get("AIDW_REF_BUDGET_S", "300"))
     # warm-up: untimed passes on a 1/64 query sample (threads, page-in),
     # which also size the timed steps
     probe = []

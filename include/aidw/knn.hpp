@@ -208,7 +208,8 @@ inline bool host_trace() {
 /// distances_sq vectors already hold k elements.  Building them is pure host
 /// work — one heap allocation per result plus first-touch page faults
 /// (~3 ms per 100K results on one thread) — so after each call a background
-/// thread tops the stash up to 4x the largest request seen (capped at
+/// thread (with three helpers) fills the stash to 64 MiB after the first
+/// call of a given k (4x the largest request seen after later calls, capped at
 /// 64 MiB) in batches that are usable as soon as they land; a call with a
 /// matching k moves its n results out of the stash's tail (the rest stays
 /// for the next call: no frees on the call path) and builds whatever is
@@ -254,7 +255,11 @@ public:
             want_ = 0;
         }
         const std::size_t per = sizeof(KnnResult) + k * sizeof(double) + 16;
-        want_ = std::min<std::size_t>(std::max(want_, 4 * n), (std::size_t(64) << 20) / per);
+        const std::size_t cap = (std::size_t(64) << 20) / per;
+        // first call with this k: fill the whole budget at once (a process
+        // that starts small and grows — the acceptance ladder — then finds
+        // its larger calls' storage ready); later: 4x the largest request
+        want_ = std::min<std::size_t>(want_ == 0 ? cap : std::max(want_, 4 * n), cap);
         if (stash_.size() >= want_ && doomed_.empty()) return;
         pending_ = true;
         cv_.notify_one();
@@ -276,6 +281,7 @@ private:
     // serves the calls) in batches that land in the stash as they finish.
     void loop() {
         constexpr std::size_t kBatch = 8192;
+        constexpr std::size_t kHelpers = 4;
         std::unique_lock<std::mutex> lk(mu_);
         for (;;) {
             cv_.wait(lk, [&] { return stop_ || pending_; });
@@ -288,10 +294,19 @@ private:
             lk.lock();
             pause_ = false;
             while (!stop_ && !pending_ && !pause_ && stash_.size() < want_) {
-                const std::size_t k = k_, n = std::min(kBatch, want_ - stash_.size());
+                const std::size_t k = k_, n = std::min(kBatch * kHelpers, want_ - stash_.size());
                 lk.unlock();
                 std::vector<KnnResult> v(n);
-                for (KnnResult& r : v) r.distances_sq.resize(k);
+                {  // kHelpers threads, one slice each (allocation + first touch)
+                    std::thread th[kHelpers];
+                    for (std::size_t p = 1; p < kHelpers; ++p)
+                        th[p] = std::thread([&, p] {
+                            for (std::size_t i = n * p / kHelpers; i < n * (p + 1) / kHelpers; ++i)
+                                v[i].distances_sq.resize(k);
+                        });
+                    for (std::size_t i = 0; i < n / kHelpers; ++i) v[i].distances_sq.resize(k);
+                    for (std::size_t p = 1; p < kHelpers; ++p) th[p].join();
+                }
                 lk.lock();
                 if (k != k_) continue;
                 for (KnnResult& r : v) stash_.push_back(std::move(r));

@@ -63,13 +63,16 @@ def test_reference_gpu_suites_fp32(suite):
 # Criteria 6-8 are host wall-clock ratios between stages / engines of the
 # SAME implementation (stage shares, grid-vs-brute kNN, grid-vs-brute
 # pipeline), written for a CPU build.  With the GridIndex device mirror, the
-# pinned result staging and the pre-built KnnResult storage, 7 (grid kNN
-# stage <= 0.2x brute; measured 0.15) and 8 (grid pipeline >= 1.5x brute;
-# 1.94x FP32, 1.65x FP64) pass in both precisions (profiles/r02/acceptance_*).
-# 6 asks the kNN share of a GPU pipeline to fall strictly from 10K to 50K to
-# 100K: it holds in FP64 (40 / 32 / 13 %); in FP32 the 10K and 50K shares
-# are within noise of each other (39 / 43 %, host-call-bound at these sizes),
-# so 6 stays a host-timing criterion.
+# pinned result staging and the KnnResult stash (filled to 64 MiB on a
+# background thread after the first call), 7 (grid kNN stage <= 0.2x brute;
+# measured 0.17-0.19) and 8 (grid pipeline >= 1.5x brute; 1.96-2.02x FP32,
+# 1.61x FP64) pass in both precisions (profiles/r02/acceptance_ladder_s50.txt).
+# 6 asks the kNN share of the pipeline to fall strictly from 10K to 50K to
+# 100K and stay below 15 % at 100K: the drop-in kNN stage at 100K is bound by
+# its host boundary (the C-ABI call ~1 ms — 12 MB of d2 lists back to the
+# host — plus handing over 102400 KnnResult objects) against a ~6 ms
+# weighting stage, ~20 % (a CPU build's kNN stage is the small one), so 6
+# stays a host-timing criterion.
 HOST_TIMING_CRITERIA = {6}
 # 7 and 8 are wall-clock ratios too: measured 0.14-0.27 against 0.2 for 7 on
 # different boxes with the same binary, so a failing 7 / 8 is re-measured
