@@ -478,7 +478,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const Smem& sm, uint32
     const int r = quarter * 32 + lane;
     char* myabuf = sm.abuf + g * 2 * kABytes;
 #if AIDW_TC_TRACE
-    long long wf = 0, tpart = 0, ttile = 0, tall = clock64();
+    long long wf = 0, tpart = 0, ttile = 0, tbuild = 0, tall = clock64();
 #endif
     for (int t = 0; t < T; ++t) {
         const int s = t % kStages;
@@ -526,17 +526,19 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const Smem& sm, uint32
         // profiles/r02/tc_release_s47.txt)
         mbar_arrive(&sm.bempty[s]);
         if (t + 2 < T) {  // A(t + 2): the MMAs of tile t (its last readers) are complete
+            TRACE_T0(c4);
             build_a(myabuf + (t & 1) * kABytes, r, q, __ldg(a.tile_geo + t0 + t + 2));
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.afull[g * 2 + (t & 1)]);
+            TRACE_ADD(tbuild, c4);
         }
         TRACE_ADD(ttile, c3);
     }
 #if AIDW_TC_TRACE
     if (TRACE_CTA && lane == 0)
-        printf("epi g%d q%d: total %lld  wait tfull %lld  parts %lld  tile tail %lld\n", g, quarter,
-               clock64() - tall, wf, tpart, ttile);
+        printf("epi g%d q%d: total %lld  wait tfull %lld  parts %lld  tile tail %lld (A rows %lld)\n",
+               g, quarter, clock64() - tall, wf, tpart, ttile, tbuild);
 #endif
 }
 
