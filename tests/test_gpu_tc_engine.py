@@ -102,3 +102,68 @@ def test_values_spanning_zero_and_large_magnitudes():
     out64 = A.run_pipeline(d, q, A.RunConfig(params=A.AidwParams(k=10)))
     ref0 = O.pipeline(data.xs, data.ys, zs, q.xs, q.ys, k=10, variant=0)
     assert np.max(np.abs(out64.result.predicted - ref0["pred"]) / np.abs(ref0["pred"])) <= 2e-11
+
+
+# ------------------------------------------------------------ invariances
+def test_shard_invariant():
+    """A query's bits do not depend on the other queries (its CTA, TMEM
+    lane, warp-mates, class region): the multi-GPU argument, on the
+    tensor-core engine."""
+    data = A.generate_clustered(M, seed=31)
+    q = A.generate_random_queries(6000, UNIT, 32)
+    bb = O.compute_bbox(data.xs, data.ys, q.xs, q.ys)
+    cfg = A.RunConfig(params=A.AidwParams(k=10), bbox=tuple(bb))
+    full = A.run_pipeline(data, q, cfg).result
+    assert 0.05 < np.mean(full.alphas == 4.0) < 0.95  # both K4 regions populated
+    for lo, hi in ((0, 3000), (3000, 6000), (1234, 1240), (5999, 6000)):
+        part = A.run_pipeline(data, A.PointSet(q.xs[lo:hi], q.ys[lo:hi]), cfg).result
+        assert np.array_equal(part.predicted, full.predicted[lo:hi])
+        assert np.array_equal(part.alphas, full.alphas[lo:hi])
+
+
+def test_query_slabs_bit_identical():
+    """Queries in slabs (bounded partial sums for any n): the slab bounds cut
+    through the tensor-core recipe region and the general region."""
+    data = A.generate_clustered(M, seed=33)
+    q = A.generate_random_queries(10_000, UNIT, 34)
+    cfg = A.RunConfig(params=A.AidwParams(k=10))
+    try:
+        A.set_query_slab(0)
+        ref = A.run_pipeline(data, q, cfg).result
+        for slab in (3072, 1000):
+            A.set_query_slab(slab)
+            got = A.run_pipeline(data, q, cfg).result
+            assert np.array_equal(got.predicted, ref.predicted)
+            assert np.array_equal(got.alphas, ref.alphas)
+    finally:
+        A.set_query_slab(0)
+
+
+def test_graph_replay_bit_identical():
+    data = A.generate_random_points(M, UNIT, 35)
+    q = A.generate_random_queries(5_000, UNIT, 36)
+    cfg = A.RunConfig(params=A.AidwParams(k=10))
+    A.set_graphs(False)
+    try:
+        ref = A.run_pipeline(data, q, cfg).result
+    finally:
+        A.set_graphs(True)
+    for _ in range(3):
+        got = A.run_pipeline(data, q, cfg).result
+        assert np.array_equal(got.predicted, ref.predicted)
+
+
+def test_multidevice_shards_bit_identical():
+    """Single-process multi-device path (query shards on three streams of
+    device 0, data replicated by NCCL) on the tensor-core engine."""
+    data = A.generate_random_points(M, UNIT, 37)
+    q = A.generate_random_queries(20_001, UNIT, 38)
+    cfg = A.RunConfig(params=A.AidwParams(k=10))
+    one = A.run_pipeline(data, q, cfg).result
+    A.set_devices([0, 0, 0])
+    try:
+        multi = A.run_pipeline(data, q, cfg).result
+    finally:
+        A.set_devices([])
+    assert np.array_equal(multi.predicted, one.predicted)
+    assert np.array_equal(multi.alphas, one.alphas)
