@@ -204,17 +204,16 @@ inline bool host_trace() {
     return on;
 }
 
-/// Host-side result storage of knn_stage: KnnResult objects whose
-/// distances_sq vectors already hold k elements.  Building them is pure host
-/// work — one heap allocation per result plus first-touch page faults
-/// (~3 ms per 100K results on one thread) — so after each call a background
-/// thread (with three helpers) fills the stash to 64 MiB after the first
-/// call of a given k (4x the largest request seen after later calls, capped at
-/// 64 MiB) in batches that are usable as soon as they land; a call with a
-/// matching k moves its n results out of the stash's tail (the rest stays
-/// for the next call: no frees on the call path) and builds whatever is
-/// missing on the host pool while the device runs the stage (the top-up
-/// pauses meanwhile).
+/// Host-side result storage of knn_stage: whole result vectors (n
+/// KnnResult objects whose distances_sq already hold k elements) built
+/// ahead of the call that needs them.  Building one is pure host work — an
+/// allocation and first-touch page faults per result, ~3 ms per 100K on one
+/// thread — so after each call of shape (n, k) a background thread (with
+/// three helpers) builds vectors of n and 2n results (a repeated shape, or
+/// a growing one such as the acceptance ladder's 10K -> 50K -> 100K), at
+/// most 64 MiB in all, and a call whose (n, k) matches takes one in O(1).
+/// Otherwise the storage is built on the host pool while the device runs
+/// the stage.
 class ResultStash {
 public:
     static ResultStash& instance() {
@@ -222,45 +221,41 @@ public:
         return stash;
     }
 
-    /// n results with distances_sq.size() == k: the stash's tail, and what
-    /// it lacks built on the host pool (the background top-up pauses).
+    /// n results with distances_sq.size() == k.
     std::vector<KnnResult> take(std::size_t n, std::size_t k) {
-        std::vector<KnnResult> v;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            if (k_ == k && !stash_.empty()) {
-                const std::size_t got = std::min(n, stash_.size());
-                v.assign(std::make_move_iterator(stash_.end() - got),
-                         std::make_move_iterator(stash_.end()));
-                stash_.erase(stash_.end() - got, stash_.end());
-            }
-            if (v.size() < n) pause_ = true;
+            for (auto it = ready_.begin(); it != ready_.end(); ++it)
+                if (it->size() == n && k_ == k) {
+                    std::vector<KnnResult> v = std::move(*it);
+                    ready_.erase(it);
+                    return v;
+                }
         }
-        if (v.size() == n) return v;
-        const std::size_t have = v.size();
-        v.resize(n);
-        HostPool::instance().parallel_for(n - have, 4096, [&](std::size_t lo, std::size_t hi) {
-            for (std::size_t i = have + lo; i < have + hi; ++i) v[i].distances_sq.resize(k);
+        std::vector<KnnResult> v(n);
+        HostPool::instance().parallel_for(n, 4096, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t i = lo; i < hi; ++i) v[i].distances_sq.resize(k);
         });
         return v;
     }
 
-    /// Schedule the top-up after a call of shape (n, k).
+    /// Schedule vectors for the next calls after a call of shape (n, k).
     void refill(std::size_t n, std::size_t k) {
         std::lock_guard<std::mutex> lk(mu_);
         if (k != k_) {
-            doomed_.push_back(std::move(stash_));  // freed on the worker, off the call path
-            stash_.clear();
+            for (auto& v : ready_) doomed_.push_back(std::move(v));  // freed on the worker
+            ready_.clear();
             k_ = k;
-            want_ = 0;
         }
         const std::size_t per = sizeof(KnnResult) + k * sizeof(double) + 16;
         const std::size_t cap = (std::size_t(64) << 20) / per;
-        // first call with this k: fill the whole budget at once (a process
-        // that starts small and grows — the acceptance ladder — then finds
-        // its larger calls' storage ready); later: 4x the largest request
-        want_ = std::min<std::size_t>(want_ == 0 ? cap : std::max(want_, 4 * n), cap);
-        if (stash_.size() >= want_ && doomed_.empty()) return;
+        want_.clear();
+        for (std::size_t size : {n, 2 * n}) {
+            bool have = false;
+            for (const auto& v : ready_) have |= v.size() == size;
+            if (!have && size > 0 && size <= cap) want_.push_back(size);
+        }
+        if (want_.empty() && doomed_.empty()) return;
         pending_ = true;
         cv_.notify_one();
     }
@@ -277,11 +272,21 @@ public:
 private:
     ResultStash() : worker_([this] { loop(); }) {}
 
-    // The top-up runs on this one worker thread (never the host pool, which
-    // serves the calls) in batches that land in the stash as they finish.
+    static std::vector<KnnResult> build_background(std::size_t n, std::size_t k) {
+        constexpr std::size_t kHelpers = 4;  // this thread + three
+        std::vector<KnnResult> v(n);
+        std::thread th[kHelpers];
+        for (std::size_t p = 1; p < kHelpers; ++p)
+            th[p] = std::thread([&, p] {
+                for (std::size_t i = n * p / kHelpers; i < n * (p + 1) / kHelpers; ++i)
+                    v[i].distances_sq.resize(k);
+            });
+        for (std::size_t i = 0; i < n / kHelpers; ++i) v[i].distances_sq.resize(k);
+        for (std::size_t p = 1; p < kHelpers; ++p) th[p].join();
+        return v;
+    }
+
     void loop() {
-        constexpr std::size_t kBatch = 8192;
-        constexpr std::size_t kHelpers = 4;
         std::unique_lock<std::mutex> lk(mu_);
         for (;;) {
             cv_.wait(lk, [&] { return stop_ || pending_; });
@@ -289,37 +294,36 @@ private:
             pending_ = false;
             std::vector<std::vector<KnnResult>> doomed = std::move(doomed_);
             doomed_.clear();
+            const std::vector<std::size_t> sizes = want_;
+            const std::size_t k = k_;
             lk.unlock();
             doomed.clear();
-            lk.lock();
-            pause_ = false;
-            while (!stop_ && !pending_ && !pause_ && stash_.size() < want_) {
-                const std::size_t k = k_, n = std::min(kBatch * kHelpers, want_ - stash_.size());
-                lk.unlock();
-                std::vector<KnnResult> v(n);
-                {  // kHelpers threads, one slice each (allocation + first touch)
-                    std::thread th[kHelpers];
-                    for (std::size_t p = 1; p < kHelpers; ++p)
-                        th[p] = std::thread([&, p] {
-                            for (std::size_t i = n * p / kHelpers; i < n * (p + 1) / kHelpers; ++i)
-                                v[i].distances_sq.resize(k);
-                        });
-                    for (std::size_t i = 0; i < n / kHelpers; ++i) v[i].distances_sq.resize(k);
-                    for (std::size_t p = 1; p < kHelpers; ++p) th[p].join();
-                }
+            for (std::size_t size : sizes) {
+                std::vector<KnnResult> v = build_background(size, k);
                 lk.lock();
-                if (k != k_) continue;
-                for (KnnResult& r : v) stash_.push_back(std::move(r));
+                std::vector<std::vector<KnnResult>> evicted;
+                if (k == k_) {  // oldest vectors make room: 64 MiB in all
+                    const std::size_t per = sizeof(KnnResult) + k * sizeof(double) + 16;
+                    std::size_t held = size;
+                    for (const auto& r : ready_) held += r.size();
+                    while (held * per > (std::size_t(64) << 20) && !ready_.empty()) {
+                        held -= ready_.front().size();
+                        evicted.push_back(std::move(ready_.front()));
+                        ready_.erase(ready_.begin());
+                    }
+                    ready_.push_back(std::move(v));
+                }
+                lk.unlock();  // evicted (or a stale v) freed here, off the lock
             }
+            lk.lock();
         }
     }
 
     std::mutex mu_;
     std::condition_variable cv_;
-    bool pause_ = false;
-    std::vector<KnnResult> stash_;
-    std::vector<std::vector<KnnResult>> doomed_;
-    std::size_t k_ = 0, want_ = 0;
+    std::vector<std::vector<KnnResult>> ready_, doomed_;
+    std::vector<std::size_t> want_;
+    std::size_t k_ = 0;
     bool pending_ = false, stop_ = false;
     std::thread worker_;
 };
