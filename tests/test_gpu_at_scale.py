@@ -208,6 +208,28 @@ def test_pipeline_1m_stratified_sample():
     assert rel_err(out64.result.predicted[s], ref_pred) <= FP64_TOL
 
 
+# ------------------------------------------------------------------ IDW at scale
+@pytest.mark.parametrize("alpha", [2.0, 2.5])
+def test_idw_1m_sample(alpha):
+    """Constant-alpha IDW over 1M points (idw_predict_all, interpolate.hpp:426-448;
+    alpha = 2: the reference's default exponent, one tensor-core recipe
+    class; 2.5: the general form on the CUDA cores): all 1M queries on the
+    GPU, 4096 of them spread over the index range against the reference's
+    run_pipeline in idw mode, plus the bbox-pinning queries."""
+    need_ref()
+    xs, ys, zs = O.generate_points(1_000_000, UNIT, 42)
+    qx, qy = O.generate_queries(1_000_000, UNIT, 43)
+    out = A.run_pipeline(A.PointSet(xs, ys, zs), A.PointSet(qx, qy),
+                         A.RunConfig(mode="idw", alpha=alpha))
+    s = np.unique(np.concatenate([np.arange(0, qx.size, qx.size // 4096),
+                                  [np.argmin(qx), np.argmax(qx), np.argmin(qy), np.argmax(qy)]]))
+    assert np.array_equal(O.compute_bbox(xs, ys, qx[s], qy[s]), O.compute_bbox(xs, ys, qx, qy))
+    ref_pred, _, _, _ = O.ref_run_pipeline(xs, ys, zs, qx[s], qy[s], mode=0, alpha=alpha,
+                                           workers=THREADS)
+    assert pred_err(out.result.predicted[s], ref_pred, zs) <= FP32_TOL
+    assert np.all(out.result.alphas == alpha)
+
+
 # ------------------------------------------------------------------ DEM kNN, full
 def test_dem_knn_stage_all_lattice_queries():
     """configs[4] kNN in full: all 4096^2 lattice queries over 4M planar
