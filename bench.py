@@ -417,6 +417,11 @@ def main():
     local = 0 if shared else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # everything on one non-default stream: the L2 flush, the inputs and the
+    # library's work are stream-ordered (a NULL stream handle would make the
+    # library use its own stream, not ordered after the flush), and the
+    # events time exactly that stream
+    torch.cuda.set_stream(torch.cuda.Stream(dev))
     if world > 1:
         if shared:
             dist.init_process_group("gloo")

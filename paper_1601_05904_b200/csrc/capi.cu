@@ -131,6 +131,15 @@ std::string locate_msg(double x, double y) {  // grid.hpp:100-101
            ") lies outside the covered region";
 }
 
+// AIDW_HOST_TRACE=1: host-side phase times of each fused pass on stderr.
+bool host_trace() {
+    static const bool on = [] {
+        const char* v = std::getenv("AIDW_HOST_TRACE");
+        return v && *v == '1';
+    }();
+    return on;
+}
+
 // ------------------------------------------------------------ device context
 std::once_flag g_pool_once[64];
 size_t g_pool_keep[64];  // the pool's release threshold per device
@@ -139,11 +148,17 @@ void* pinned_alloc(size_t bytes);
 void pinned_free(void* p);
 
 int current_device() {
-    int count = 0;
-    cudaError_t e = cudaGetDeviceCount(&count);
-    if (e != cudaSuccess || count == 0)
-        throw Failure(AIDW_ERR_CUDA, std::string("no CUDA device available: ") +
-                                          (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+    // the device count is asked once per process (cudaGetDeviceCount costs
+    // ~50 us a call — a seventh of a 10K x 10K pass)
+    static std::atomic<int> known{0};
+    if (known.load(std::memory_order_relaxed) == 0) {
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0)
+            throw Failure(AIDW_ERR_CUDA, std::string("no CUDA device available: ") +
+                                              (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+        known.store(count, std::memory_order_relaxed);
+    }
     int dev = 0;
     CK(cudaGetDevice(&dev));
     std::call_once(g_pool_once[dev & 63], [dev] {
@@ -172,24 +187,40 @@ int current_device() {
     return dev;
 }
 
+// The stream of a call: the caller's, or (stream == NULL) the library's own
+// non-blocking stream for this host thread and device — created once and
+// kept (creating and destroying one per call cost ~50 us, an eighth of a
+// 10K x 10K pass); a call on it is synchronous (the stream is drained
+// before the call returns).
+struct ManagedStreams {
+    cudaStream_t s[64] = {};
+    ~ManagedStreams() {  // thread exit: no stream outlives its thread
+        for (cudaStream_t& x : s)
+            if (x) cudaStreamDestroy(x);
+    }
+};
+cudaStream_t managed_stream(int dev) {
+    thread_local ManagedStreams streams;
+    cudaStream_t& s = streams.s[dev & 63];
+    if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
 struct StreamScope {
     cudaStream_t s = nullptr;
     bool own = false;
     explicit StreamScope(void* external = nullptr) {
-        current_device();
+        const int dev = current_device();
         if (external) {
             s = static_cast<cudaStream_t>(external);
         } else {
-            CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            s = managed_stream(dev);
             own = true;
         }
     }
     void sync() { CK(cudaStreamSynchronize(s)); }
     ~StreamScope() {
-        if (own) {
-            cudaStreamSynchronize(s);
-            cudaStreamDestroy(s);
-        }
+        if (own) cudaStreamSynchronize(s);
     }
 };
 
@@ -881,10 +912,14 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
                     cudaStream_t s, double h2d_ms, const std::chrono::steady_clock::time_point& t0,
                     double* h_pred, double* h_alpha) {
     const long long launches0 = g_launches.load();
+    const auto ta = std::chrono::steady_clock::now();
     MaybeArena arena(s);  // declared first: destroyed after every DBuf of the call
+    const auto tb = std::chrono::steady_clock::now();
     aidw_run_stats local{};
     DBuf<double> hull(6, s);
+    const auto tp0 = std::chrono::steady_clock::now();
     const PassPlan pl = plan_pass(io, cfg, &local, hull.get(), s);
+    const auto tp1 = std::chrono::steady_clock::now();
     FailFlags fails(s, /*defer_init=*/true);
     PassEvents eager;
     struct EventsGuard {
@@ -892,6 +927,7 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
         ~EventsGuard() { e.destroy(); }
     } guard{eager};
     const PassEvents& ev = run_pass(pl, io, cfg, fails, eager, t_arena, s);
+    const auto tp2 = std::chrono::steady_clock::now();
     double d2h_ms = 0.0;
     if (h_pred) {
         const auto c0 = std::chrono::steady_clock::now();
@@ -901,6 +937,13 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
         d2h_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
     }
     fails.fetch(s);  // failure indices and pass counters, one copy
+    if (host_trace()) {
+        const auto tp3 = std::chrono::steady_clock::now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "[aidw pass] m %zu n %zu: entry %.1f, arena %.1f, hull %.1f, plan %.1f, "
+                     "enqueue %.1f, wait+fetch %.1f us\n", io.m, io.n, us(t0, ta), us(ta, tb),
+                     us(tb, tp0), us(tp0, tp1), us(tp1, tp2), us(tp2, tp3));
+    }
     raise_pass_failures(fails);
     if (st) {
         *st = local;
