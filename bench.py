@@ -647,11 +647,14 @@ def main():
             return A.run_pipeline(hd, hq, hcfg, out=pout)
     e2e_call()
     barrier()
+    # at least --e2e-steps calls and ~0.3 s of them (small configs: host-clock noise)
+    e2e_steps = max(args.e2e_steps, int(np.ceil(0.3 / max(ms_per_step / 1e3, 1e-6))))
+    e2e_steps = int(allmax(e2e_steps))
     t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
+    for _ in range(e2e_steps):
         e2e_call()
     barrier()
-    e2e_s = allmax((time.perf_counter() - t0) / args.e2e_steps)
+    e2e_s = allmax((time.perf_counter() - t0) / e2e_steps)
     e2e_value = job.n_total / e2e_s
 
     cpu = None
@@ -726,7 +729,7 @@ def main():
                     "api": "aidw_run_raster (C-ABI)" if raster_e2e else "aidw_run_pipeline (C-ABI)",
                     "h2d_bytes_per_step": 24 * m + (0 if raster_e2e else 16 * n),
                     "d2h_bytes_per_step": (8 if raster_e2e else 16) * n,
-                    "s_per_step": e2e_s},
+                    "s_per_step": e2e_s, "calls": e2e_steps},
             "gpu_launches": launches,
             "cuda_graphs": A.graph_counters(),
             "clocks": clk,

@@ -206,6 +206,27 @@ cudaStream_t managed_stream(int dev) {
     return s;
 }
 
+// A pair of timing events for this host thread and the current device
+// (the uploads of aidw_run_pipeline), created once.
+struct ThreadEvents {
+    cudaEvent_t b[64] = {}, e[64] = {};
+    ~ThreadEvents() {
+        for (int i = 0; i < 64; ++i) {
+            if (b[i]) cudaEventDestroy(b[i]);
+            if (e[i]) cudaEventDestroy(e[i]);
+        }
+    }
+};
+void h2d_events(cudaEvent_t& b, cudaEvent_t& e) {
+    thread_local ThreadEvents ev;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!ev.b[dev & 63]) CK(cudaEventCreate(&ev.b[dev & 63]));
+    if (!ev.e[dev & 63]) CK(cudaEventCreate(&ev.e[dev & 63]));
+    b = ev.b[dev & 63];
+    e = ev.e[dev & 63];
+}
+
 struct StreamScope {
     cudaStream_t s = nullptr;
     bool own = false;
@@ -929,14 +950,14 @@ void pipeline_entry(const PipelineIO& io, const aidw_run_config& cfg, aidw_run_s
     const PassEvents& ev = run_pass(pl, io, cfg, fails, eager, t_arena, s);
     const auto tp2 = std::chrono::steady_clock::now();
     double d2h_ms = 0.0;
-    if (h_pred) {
-        const auto c0 = std::chrono::steady_clock::now();
+    const auto c0 = std::chrono::steady_clock::now();
+    if (h_pred) {  // results and the failure flags come back behind one synchronisation
         d2h(h_pred, io.pred, io.n, s);
         if (h_alpha) d2h(h_alpha, io.alpha, io.n, s);
-        CK(cudaStreamSynchronize(s));
-        d2h_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
     }
     fails.fetch(s);  // failure indices and pass counters, one copy
+    if (h_pred)
+        d2h_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
     if (host_trace()) {
         const auto tp3 = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
@@ -1778,17 +1799,21 @@ int aidw_run_pipeline(const double* dx, const double* dy, const double* dz, size
         cudaStream_t s = ss.s;
         ArenaScope arena(s);  // uploads in the call's workspace too (graph-replayable)
         DBuf<double> ddx, ddy, ddz, dqx, dqy, pred(n, s), alpha(n, s);
+        // the uploads are timed by events on the stream (no synchronisation
+        // between them and the pass)
+        cudaEvent_t h2d_b, h2d_e;
+        h2d_events(h2d_b, h2d_e);
+        CK(cudaEventRecord(h2d_b, s));
         h2d(ddx, dx, m, s);
         h2d(ddy, dy, m, s);
         if (dz) h2d(ddz, dz, m, s);
         h2d(dqx, qx, n, s);
         h2d(dqy, qy, n, s);
-        ss.sync();
-        const double h2d_ms =
-            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        CK(cudaEventRecord(h2d_e, s));
         PipelineIO io{ddx.get(), ddy.get(), dz ? ddz.get() : nullptr, dqx.get(), dqy.get(), m, n,
                       pred.get(), alpha.get()};
-        pipeline_entry(io, *cfg, stats, s, h2d_ms, t0, pred_out, alpha_out);
+        pipeline_entry(io, *cfg, stats, s, 0.0, t0, pred_out, alpha_out);
+        if (stats) stats->h2d_ms = Events::ms(h2d_b, h2d_e);  // complete: the call synchronised
     });
 }
 
