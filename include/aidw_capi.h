@@ -245,7 +245,8 @@ int aidw_run_pipeline(const double* dx, const double* dy, const double* dz, size
                       aidw_error* err);
 
 /* Same pipeline over DEVICE-resident inputs/outputs (current device).
- * `stream` is a cudaStream_t (NULL = the library's own stream). */
+ * `stream` is a cudaStream_t (NULL = the library's own stream, ordered after
+ * the work already queued on the legacy default stream). */
 int aidw_run_pipeline_device(const double* d_dx, const double* d_dy, const double* d_dz,
                              size_t m, const double* d_qx, const double* d_qy, size_t n,
                              const aidw_run_config* cfg, double* d_pred, double* d_alpha,

@@ -191,18 +191,31 @@ int current_device() {
 // non-blocking stream for this host thread and device — created once and
 // kept (creating and destroying one per call cost ~50 us, an eighth of a
 // 10K x 10K pass); a call on it is synchronous (the stream is drained
-// before the call returns).
+// before the call returns) and starts after the legacy default stream's
+// queued work.
+// The call is ordered after work already queued on the legacy default
+// stream (e.g. the caller's cudaMemcpyAsync(..., 0) of a device input): one
+// event recorded there, waited on by the library's stream.
 struct ManagedStreams {
     cudaStream_t s[64] = {};
+    cudaEvent_t legacy[64] = {};
     ~ManagedStreams() {  // thread exit: no stream outlives its thread
-        for (cudaStream_t& x : s)
-            if (x) cudaStreamDestroy(x);
+        for (int i = 0; i < 64; ++i) {
+            if (s[i]) cudaStreamDestroy(s[i]);
+            if (legacy[i]) cudaEventDestroy(legacy[i]);
+        }
     }
 };
 cudaStream_t managed_stream(int dev) {
     thread_local ManagedStreams streams;
     cudaStream_t& s = streams.s[dev & 63];
-    if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEvent_t& e = streams.legacy[dev & 63];
+    if (!s) {
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(e, cudaStreamLegacy));
+    CK(cudaStreamWaitEvent(s, e, 0));
     return s;
 }
 
