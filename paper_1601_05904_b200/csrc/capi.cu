@@ -148,9 +148,7 @@ void* pinned_alloc(size_t bytes);
 void pinned_free(void* p);
 
 int current_device() {
-    // the device count is asked once per process (cudaGetDeviceCount costs
-    // ~50 us a call — a seventh of a 10K x 10K pass)
-    static std::atomic<int> known{0};
+    static std::atomic<int> known{0};  // the device count, asked until a device is found
     if (known.load(std::memory_order_relaxed) == 0) {
         int count = 0;
         cudaError_t e = cudaGetDeviceCount(&count);
@@ -191,11 +189,9 @@ int current_device() {
 // non-blocking stream for this host thread and device — created once and
 // kept (creating and destroying one per call cost ~50 us, an eighth of a
 // 10K x 10K pass); a call on it is synchronous (the stream is drained
-// before the call returns) and starts after the legacy default stream's
-// queued work.
-// The call is ordered after work already queued on the legacy default
-// stream (e.g. the caller's cudaMemcpyAsync(..., 0) of a device input): one
-// event recorded there, waited on by the library's stream.
+// before the call returns) and starts after the work already queued on the
+// legacy default stream (e.g. the caller's cudaMemcpyAsync(..., 0) of a
+// device input): one event recorded there, waited on by the library's stream.
 struct ManagedStreams {
     cudaStream_t s[64] = {};
     cudaEvent_t legacy[64] = {};
