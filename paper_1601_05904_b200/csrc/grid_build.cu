@@ -697,13 +697,21 @@ constexpr int kBucketMaxBits = 12;
 constexpr int kBucketThreads = 1024;
 constexpr int kUnroll = 8;
 constexpr size_t kSmallSortMax = 65536;
+constexpr size_t kBucketSmemMax = 200 * 1024;  // counters + copies in shared memory up to this
+// SMEM: the (key, value) copies stay in shared memory after the counters
+// (n small enough), else in the global scratch tk / tv.
+template <bool SMEM>
 __global__ void __launch_bounds__(kBucketThreads) bucket_small_kernel(uint32_t* __restrict__ keys,
                                                                       uint32_t* __restrict__ vals,
                                                                       size_t n, int shift, int nb,
                                                                       uint32_t* __restrict__ tk,
                                                                       uint32_t* __restrict__ tv) {
-    extern __shared__ uint32_t cnt[];  // nb = 2^B counters
+    extern __shared__ uint32_t cnt[];  // nb = 2^B counters (then 2n copies if SMEM)
     __shared__ uint32_t wsum[kBucketThreads / 32];
+    if (SMEM) {
+        tk = cnt + nb;
+        tv = tk + n;
+    }
     const int t = threadIdx.x;
     for (int b = t; b < nb; b += kBucketThreads) cnt[b] = 0u;
     __syncthreads();
@@ -787,11 +795,19 @@ void bucket_by_key_small(uint32_t* keys, uint32_t* vals, size_t n, int bits, cud
     const int shift = bits - b;
     const int nb = 1 << b;
     const size_t smem = static_cast<size_t>(nb) * sizeof(uint32_t);
-    CK(cudaFuncSetAttribute(bucket_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem_all = smem + 2 * n * sizeof(uint32_t);
+    if (smem_all <= kBucketSmemMax) {  // the copies in shared memory: no global round trip
+        CK(cudaFuncSetAttribute(bucket_small_kernel<true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_all)));
+        LAUNCH(bucket_small_kernel<true>, 1, kBucketThreads, smem_all, s, keys, vals, n, shift, nb,
+               static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr));
+        return;
+    }
+    CK(cudaFuncSetAttribute(bucket_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)));
     DBuf<uint32_t> tk(n, s), tv(n, s);
-    LAUNCH(bucket_small_kernel, 1, kBucketThreads, smem, s, keys, vals, n, shift, nb, tk.get(),
-           tv.get());
+    LAUNCH(bucket_small_kernel<false>, 1, kBucketThreads, smem, s, keys, vals, n, shift, nb,
+           tk.get(), tv.get());
 }
 
 size_t small_sort_n() {
