@@ -78,3 +78,47 @@ def test_pipeline_random_case_fp64(seed):
     rel = np.abs(out.result.predicted - ref["pred"]) / np.maximum(np.abs(ref["pred"]),
                                                                   1e-3 * max(span, 1e-300))
     assert float(np.max(rel)) <= 2e-11
+
+
+def case_tc(seed):
+    """Sizes where K4 runs on the tensor-core engine (m >= 64K), with random
+    levels (integer-saturating ones give the alpha = 1 / 2 / 3 recipe classes
+    and mixed warps), domains, value rules and duplicated sites."""
+    rng = np.random.default_rng(seed)
+    m = int(rng.integers(65_600, 160_000))
+    n = int(rng.choice([1, 33, 500, 1500]))
+    x0, y0 = rng.uniform(-1e3, 1e3, 2)
+    w = 10.0 ** rng.uniform(-3, 3)
+    h = w * rng.uniform(0.3, 3.0)
+    box = (x0, y0, x0 + w, y0 + h)
+    kind = rng.choice(["uniform", "planar", "clustered", "dups"])
+    if kind == "clustered":
+        xs, ys, zs = O.generate_clustered(m, seed=seed)
+        xs, ys = box[0] + xs * w, box[1] + ys * h
+    else:
+        xs, ys, zs = O.generate_points(m, box, seed, 1 if kind == "planar" else 0)
+        if kind == "dups":
+            k_d = max(1, m // 7)
+            xs[:k_d] = xs[0]
+            ys[:k_d] = ys[0]
+    qx, qy = O.generate_queries(n, box, seed + 1)
+    if rng.random() < 0.3:
+        j = rng.integers(0, m, min(n, 5))
+        qx[:j.size], qy[:j.size] = xs[j], ys[j]
+    k = int(rng.choice([1, 5, 10, 15, 32]))
+    levels = [(0.5, 1.0, 2.0, 3.0, 4.0), (1.0, 1.0, 2.0, 3.0, 4.0), (2.0, 2.0, 3.0, 4.0, 4.0),
+              (1.0, 1.5, 2.5, 3.0, 3.0)][int(rng.integers(0, 4))]
+    factor = float(rng.choice([2.0, 4.0, 8.0]))
+    return xs, ys, zs, qx, qy, k, factor, levels
+
+
+@pytest.mark.parametrize("seed", range(2000, 2060))
+def test_pipeline_random_case_tensor_core_engine(seed):
+    xs, ys, zs, qx, qy, k, factor, levels = case_tc(seed)
+    assert A.weight_engine(xs.size) == "tensor-core"
+    out = A.run_pipeline(A.PointSet(xs, ys, zs), A.PointSet(qx, qy),
+                         A.RunConfig(params=A.AidwParams(k=k, alpha_levels=levels),
+                                     cell_factor=factor))
+    ref = O.pipeline(xs, ys, zs, qx, qy, k=k, factor=factor, variant=1, levels=levels)
+    assert np.max(np.abs(out.result.alphas - ref["alpha"]) / ref["alpha"]) <= 1e-12
+    assert pred_err(out.result.predicted, ref["pred"], zs) <= 1e-5
