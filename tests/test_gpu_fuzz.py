@@ -121,4 +121,14 @@ def test_pipeline_random_case_tensor_core_engine(seed):
                                      cell_factor=factor))
     ref = O.pipeline(xs, ys, zs, qx, qy, k=k, factor=factor, variant=1, levels=levels)
     assert np.max(np.abs(out.result.alphas - ref["alpha"]) / ref["alpha"]) <= 1e-12
-    assert pred_err(out.result.predicted, ref["pred"], zs) <= 1e-5
+    span = float(zs.max() - zs.min())
+    if zs.min() < 0.0 < zs.max():
+        # a zero-crossing field (planar values on a shifted domain): FP32
+        # weights leave an absolute error of ~1e-7 of the span, so the
+        # relative contract applies where |ref| >= 2 % of the span
+        # (DESIGN.md (c); seed 2048: 1.2e-8 of the span at |ref| = 0.3 %)
+        err = np.abs(out.result.predicted - ref["pred"])
+        assert err.max() <= 1e-6 * span
+        assert np.max(err / np.maximum(np.abs(ref["pred"]), 2e-2 * span)) <= 1e-5
+    else:
+        assert pred_err(out.result.predicted, ref["pred"], zs) <= 1e-5
